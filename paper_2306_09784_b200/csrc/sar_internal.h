@@ -1,0 +1,80 @@
+// Internal declarations shared by the libsar translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/sar_bp.h"
+
+namespace sar {
+
+constexpr double kLightSpeed = 299792458.0;  // m/s
+constexpr double kPi = 3.14159265358979323846;
+
+// BP pixel tile of one CTA (see bp_kernel.cu for the warp/lane -> pixel map).
+constexpr int kTileX = 32;
+constexpr int kTileY = 32;
+constexpr int kBpStages = 3;             // shared-memory ring depth
+constexpr int kBpMaxItemsPerStage = 32;  // (chirp, rx) windows per ring stage
+constexpr int kBpStageBudgetBytes = 24 * 1024;
+
+// Range-compression kernel arguments (rc_kernel.cu).
+struct RcArgs {
+  const float* raw;        // [rows][ns], row = m * n_rx + n
+  const float* wsar;       // [n_chirps] or nullptr
+  const float* window;     // [ns] range window (plan table)
+  const float2* twiddle;   // [nfft/2] exp(-j 2 pi q / nfft) (plan table)
+  const float2* ramp;      // [n_bins] exp(+j 2 pi k t_c / nfft), k = k_lo + i (plan table)
+  float2* prof;            // [rows][n_bins]
+  int row0, nrows;         // rows of the chirp shard
+  int n_rx, ns, nfft, log2n, k_lo, n_bins;
+  float scale;             // 2 / sum(window)
+};
+
+// Back-projection kernel arguments (bp_kernel.cu).
+struct BpArgs {
+  const float2* prof;      // [n_chirps][n_rx][n_bins]
+  const double* tx;        // [n_chirps][3]
+  const double* rx;        // [n_chirps][n_rx][3] or nullptr (monostatic)
+  const float* dop;        // [ny][nx] or nullptr
+  float2* img;             // [nrow][nx]
+  int n_bins, n_rx, chirp0, nchirp, row0, nrow, nx, tiles_x, accumulate;
+  int W;                   // window bins per item
+  int CB;                  // chirps per ring stage
+  double x0, y0, z0, dx, dy;
+  double a1, c2, k_lo;     // bins / metre two-way, cycles / metre two-way, crop start
+  double kap_half;         // half window span in bins: 2 a1 rho + doppler bound
+  float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
+  float C2f;               // phase slope (rad) per metre of Delta-R
+};
+
+size_t bp_smem_bytes(int W, int CB, int n_rx, bool bistatic);
+cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
+cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s);
+
+}  // namespace sar
+
+struct sar_plan_s {
+  sar_radar_params_t radar;
+  sar_grid_t grid;
+  sar_box_t box;
+  sar_plan_info_t info;
+  int device;
+  bool near_field;         // an antenna may come within 2 rho of a tile anchor
+  double tile_rho;         // tile half-diagonal (m)
+  float rc_scale;
+  float* d_window = nullptr;
+  float2* d_twiddle = nullptr;
+  float2* d_ramp = nullptr;
+  // sar_form_image workspace (lazily allocated)
+  float* w_raw = nullptr;
+  float* w_wsar = nullptr;
+  double* w_tx = nullptr;
+  double* w_rx = nullptr;
+  float* w_dop = nullptr;
+  float2* w_prof = nullptr;
+  float2* w_img = nullptr;
+  std::atomic<int64_t> launches{0};
+};

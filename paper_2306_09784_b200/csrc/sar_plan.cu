@@ -1,0 +1,415 @@
+// libsar C ABI: plan maths, validation, constant tables, launches (include/sar_bp.h).
+//
+// Citations: P:Lnnn = PAPER.md line (arXiv 2306.09784); A1..A17 = readings in DESIGN.md.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sar_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sar_status_t fail(sar_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+sar_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(SAR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool finite_pos(double v) { return isfinite(v) && v > 0.0; }
+
+// Minimum and maximum Euclidean distance between two axis-aligned boxes.
+void box_distance(const double alo[3], const double ahi[3], const double blo[3],
+                  const double bhi[3], double* dmin, double* dmax) {
+  double s_min = 0.0, s_max = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const double gap = std::max(0.0, std::max(alo[k] - bhi[k], blo[k] - ahi[k]));
+    const double far = std::max(fabs(ahi[k] - blo[k]), fabs(bhi[k] - alo[k]));
+    s_min += gap * gap;
+    s_max += far * far;
+  }
+  *dmin = sqrt(s_min);
+  *dmax = sqrt(s_max);
+}
+
+struct Derived {
+  sar_plan_info_t info;
+  double rho;
+  bool near_field;
+};
+
+// Host-side plan maths shared by sar_plan_geometry and sar_plan_create.
+sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_box_t* b,
+                    Derived* out) {
+  if (!r || !g || !b || !out) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (!finite_pos(r->f0_hz) || !finite_pos(r->bandwidth_hz) || !finite_pos(r->chirp_s) ||
+      !finite_pos(r->pri_s) || !finite_pos(r->sample_rate_hz))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "radar times and frequencies must be finite and > 0");
+  if (r->pri_s < r->chirp_s) return fail(SAR_ERR_INVALID_ARGUMENT, "pri_s must be >= chirp_s");
+  if (r->n_samples < 2) return fail(SAR_ERR_INVALID_ARGUMENT, "n_samples must be >= 2");
+  if (llround(r->sample_rate_hz * r->chirp_s) != r->n_samples)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "round(sample_rate_hz * chirp_s) must equal n_samples");
+  if (r->fft_len < r->n_samples || r->fft_len > 16384 || (r->fft_len & (r->fft_len - 1)))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "fft_len must be a power of two in [n_samples, 16384]");
+  if (r->n_chirps < 1 || r->n_rx < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "n_chirps and n_rx must be >= 1");
+  if (r->range_window != 0 && r->range_window != 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "range_window must be 0 (rect) or 1 (Hann)");
+  if (!(r->doppler_max_bins >= 0.0f) || !isfinite(r->doppler_max_bins))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "doppler_max_bins must be finite and >= 0");
+  if (!finite_pos(g->dx) || !finite_pos(g->dy) || !isfinite(g->x0) || !isfinite(g->y0) ||
+      !isfinite(g->z0) || g->nx < 1 || g->ny < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "grid needs finite origin, dx, dy > 0, nx, ny >= 1");
+  for (int k = 0; k < 3; ++k)
+    if (!isfinite(b->lo[k]) || !isfinite(b->hi[k]) || b->lo[k] > b->hi[k])
+      return fail(SAR_ERR_INVALID_ARGUMENT, "antenna box needs finite lo <= hi");
+
+  sar_plan_info_t& I = out->info;
+  memset(&I, 0, sizeof(I));
+  const double N = (double)r->fft_len;
+  I.chirp_rate_hz_per_s = r->bandwidth_hz / r->chirp_s;                    // mu
+  I.a1_bins_per_m = I.chirp_rate_hz_per_s * N / (sar::kLightSpeed * r->sample_rate_hz);
+  I.c2_cycles_per_m = r->f0_hz / sar::kLightSpeed;                         // f0 / c (A3)
+
+  const double glo[3] = {g->x0, g->y0, g->z0};
+  const double ghi[3] = {g->x0 + (g->nx - 1) * g->dx, g->y0 + (g->ny - 1) * g->dy, g->z0};
+  double dist_min, dist_max;
+  box_distance(glo, ghi, b->lo, b->hi, &dist_min, &dist_max);
+  I.d_min_m = 2.0 * dist_min;  // each leg lies in [dist_min, dist_max]
+  I.d_max_m = 2.0 * dist_max;
+  const double dop = r->doppler_max_bins;
+  const long half = r->fft_len / 2;
+  long k_lo = (long)floor(I.a1_bins_per_m * I.d_min_m - dop) - 2;
+  long k_hi = (long)floor(I.a1_bins_per_m * I.d_max_m + dop) + 3;
+  k_lo = std::max(0L, std::min(k_lo, half));
+  k_hi = std::max(k_lo, std::min(k_hi, half));
+  I.k_lo = (int32_t)k_lo;
+  I.n_bins = (int32_t)(k_hi - k_lo + 1);
+
+  I.tile_x = sar::kTileX;
+  I.tile_y = sar::kTileY;
+  const double hx = 0.5 * (sar::kTileX - 1) * g->dx, hy = 0.5 * (sar::kTileY - 1) * g->dy;
+  out->rho = sqrt(hx * hx + hy * hy) * (1.0 + 1e-9) + 1e-12;
+  const double kap_half = 2.0 * I.a1_bins_per_m * out->rho + dop;
+  const double w = ceil(2.0 * kap_half) + 4.0;
+  if (w > 4096.0)
+    return fail(SAR_ERR_INVALID_ARGUMENT,
+                "pixel spacing too coarse: a 32x32 tile spans more than 4096 range bins");
+  I.window_bins = (int32_t)w;
+  const bool bistatic = r->n_rx > 1;
+  const int item_bytes = I.window_bins * 16 + 32;
+  int items = std::max(1, std::min(sar::kBpMaxItemsPerStage, sar::kBpStageBudgetBytes / item_bytes));
+  int cb = std::max(1, items / r->n_rx);
+  I.chirps_per_stage = cb;
+  (void)bistatic;
+  I.updates_per_image = (int64_t)g->nx * g->ny * r->n_chirps * r->n_rx;
+  out->near_field = dist_min < 2.0 * out->rho + 1e-3;
+  return SAR_OK;
+}
+
+template <class T>
+sar_status_t dev_alloc(T** p, size_t count) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(1, count) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SAR_ERR_NO_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return SAR_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void free_plan(sar_plan_s* p) {
+  if (!p) return;
+  cudaFree(p->d_window);
+  cudaFree(p->d_twiddle);
+  cudaFree(p->d_ramp);
+  cudaFree(p->w_raw);
+  cudaFree(p->w_wsar);
+  cudaFree(p->w_tx);
+  cudaFree(p->w_rx);
+  cudaFree(p->w_dop);
+  cudaFree(p->w_prof);
+  cudaFree(p->w_img);
+  delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sar_last_error(void) { return g_last_error.c_str(); }
+
+const char* sar_version(void) { return "libsar 0.1 (sm_100a)"; }
+
+sar_status_t sar_plan_geometry(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                               const sar_box_t* antenna_box, sar_plan_info_t* info) {
+  if (!info) return fail(SAR_ERR_INVALID_ARGUMENT, "info is null");
+  Derived d;
+  sar_status_t st = derive(radar, grid, antenna_box, &d);
+  if (st != SAR_OK) return st;
+  *info = d.info;
+  return SAR_OK;
+}
+
+sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                             const sar_box_t* antenna_box, int32_t device, sar_plan_t* out) {
+  if (!out) return fail(SAR_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  Derived d;
+  sar_status_t st = derive(radar, grid, antenna_box, &d);
+  if (st != SAR_OK) return st;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(SAR_ERR_UNSUPPORTED_DEVICE, "no such CUDA device");
+  }
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess)
+    return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(SAR_ERR_UNSUPPORTED_DEVICE,
+                std::string("libsar is built for sm_100a only; device is ") + prop.name);
+  DeviceGuard guard(device);
+  if (!guard.ok) return cuda_fail(cudaGetLastError(), "cudaSetDevice");
+
+  sar_plan_s* p = new (std::nothrow) sar_plan_s();
+  if (!p) return fail(SAR_ERR_NO_MEMORY, "host allocation failed");
+  p->radar = *radar;
+  p->grid = *grid;
+  p->box = *antenna_box;
+  p->info = d.info;
+  p->device = device;
+  p->near_field = d.near_field;
+  p->tile_rho = d.rho;
+
+  // Constant tables, computed in double and rounded once to float32.
+  const int ns = radar->n_samples, N = radar->fft_len, nb = d.info.n_bins;
+  std::vector<float> win(ns);
+  double wsum = 0.0;
+  for (int t = 0; t < ns; ++t) {
+    const double w = radar->range_window == 1 ? 0.5 - 0.5 * cos(2.0 * sar::kPi * t / (ns - 1)) : 1.0;
+    win[t] = (float)w;
+    wsum += w;
+  }
+  p->rc_scale = (float)(2.0 / wsum);  // one-sided spectrum of a real signal (A7)
+  std::vector<float2> tw(std::max(1, N / 2));
+  for (int q = 0; q < N / 2; ++q) {
+    const double a = -2.0 * sar::kPi * (double)q / (double)N;
+    tw[q] = make_float2((float)cos(a), (float)sin(a));
+  }
+  std::vector<float2> ramp(nb);
+  const double tc = 0.5 * (ns - 1);
+  for (int i = 0; i < nb; ++i) {
+    const double k = (double)(d.info.k_lo + i);
+    // exp(+j 2 pi k t_c / N); reduce k * t_c mod N exactly before scaling
+    const double ph = fmod(k * tc, (double)N) / (double)N;
+    ramp[i] = make_float2((float)cos(2.0 * sar::kPi * ph), (float)sin(2.0 * sar::kPi * ph));
+  }
+  if ((st = dev_alloc(&p->d_window, ns)) != SAR_OK || (st = dev_alloc(&p->d_twiddle, tw.size())) != SAR_OK ||
+      (st = dev_alloc(&p->d_ramp, ramp.size())) != SAR_OK) {
+    free_plan(p);
+    return st;
+  }
+  if ((e = cudaMemcpy(p->d_window, win.data(), ns * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(p->d_twiddle, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(p->d_ramp, ramp.data(), ramp.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    free_plan(p);
+    return cuda_fail(e, "cudaMemcpy (plan tables)");
+  }
+  *out = p;
+  return SAR_OK;
+}
+
+sar_status_t sar_plan_info(sar_plan_t plan, sar_plan_info_t* info) {
+  if (!plan || !info) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  *info = plan->info;
+  return SAR_OK;
+}
+
+sar_status_t sar_plan_crop(sar_plan_t plan, int32_t* k_lo, int32_t* n_bins) {
+  if (!plan || !k_lo || !n_bins) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  *k_lo = plan->info.k_lo;
+  *n_bins = plan->info.n_bins;
+  return SAR_OK;
+}
+
+int64_t sar_plan_launch_count(sar_plan_t plan) { return plan ? plan->launches.load() : -1; }
+
+sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* w_sar,
+                                int32_t chirp0, int32_t nchirp, sar_complex64_t* profiles,
+                                sar_stream_t stream) {
+  if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
+  const sar_radar_params_t& r = plan->radar;
+  if (chirp0 < 0 || nchirp < 0 || (int64_t)chirp0 + nchirp > r.n_chirps)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "chirp shard out of range");
+  if (nchirp == 0) return SAR_OK;
+  if (!raw || !profiles) return fail(SAR_ERR_INVALID_ARGUMENT, "raw and profiles must be non-null");
+  DeviceGuard guard(plan->device);
+  sar::RcArgs a;
+  a.raw = raw;
+  a.wsar = w_sar;
+  a.window = plan->d_window;
+  a.twiddle = plan->d_twiddle;
+  a.ramp = plan->d_ramp;
+  a.prof = reinterpret_cast<float2*>(profiles);
+  a.row0 = chirp0 * r.n_rx;
+  a.nrows = nchirp * r.n_rx;
+  a.n_rx = r.n_rx;
+  a.ns = r.n_samples;
+  a.nfft = r.fft_len;
+  a.log2n = 0;
+  while ((1 << a.log2n) < r.fft_len) ++a.log2n;
+  a.k_lo = plan->info.k_lo;
+  a.n_bins = plan->info.n_bins;
+  a.scale = plan->rc_scale;
+  cudaError_t e = sar::launch_rc(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "range compression launch");
+  plan->launches.fetch_add(1);
+  return SAR_OK;
+}
+
+sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
+                             const double* tx_pos, const double* rx_pos,
+                             const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                             int32_t row0, int32_t nrow, sar_complex64_t* image,
+                             int32_t accumulate, sar_stream_t stream) {
+  if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
+  const sar_radar_params_t& r = plan->radar;
+  const sar_grid_t& g = plan->grid;
+  if (chirp0 < 0 || nchirp < 0 || (int64_t)chirp0 + nchirp > r.n_chirps)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "chirp shard out of range");
+  if (row0 < 0 || nrow < 0 || (int64_t)row0 + nrow > g.ny)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "row shard out of range");
+  if (accumulate != 0 && accumulate != 1) return fail(SAR_ERR_INVALID_ARGUMENT, "accumulate must be 0 or 1");
+  if (!rx_pos && r.n_rx != 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "rx_pos may be NULL (monostatic) only when n_rx == 1");
+  if (doppler_bins && !(r.doppler_max_bins > 0.0f))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "a Doppler array needs doppler_max_bins > 0 in the plan");
+  if (nrow == 0 || (nchirp == 0 && accumulate)) return SAR_OK;
+  if (!image || (nchirp > 0 && (!profiles || !tx_pos)))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "image, profiles and tx_pos must be non-null");
+  DeviceGuard guard(plan->device);
+  sar::BpArgs a;
+  a.prof = reinterpret_cast<const float2*>(profiles);
+  a.tx = tx_pos;
+  a.rx = rx_pos;
+  a.dop = doppler_bins;
+  a.img = reinterpret_cast<float2*>(image);
+  a.n_bins = plan->info.n_bins;
+  a.n_rx = r.n_rx;
+  a.chirp0 = chirp0;
+  a.nchirp = nchirp;
+  a.row0 = row0;
+  a.nrow = nrow;
+  a.nx = g.nx;
+  a.tiles_x = (g.nx + sar::kTileX - 1) / sar::kTileX;
+  a.accumulate = accumulate;
+  a.W = plan->info.window_bins;
+  a.CB = plan->info.chirps_per_stage;
+  a.x0 = g.x0;
+  a.y0 = g.y0;
+  a.z0 = g.z0;
+  a.dx = g.dx;
+  a.dy = g.dy;
+  a.a1 = plan->info.a1_bins_per_m;
+  a.c2 = plan->info.c2_cycles_per_m;
+  a.k_lo = plan->info.k_lo;
+  a.kap_half = 2.0 * a.a1 * plan->tile_rho + (double)r.doppler_max_bins;
+  const bool bistatic = rx_pos != nullptr;
+  a.A1f = (float)(bistatic ? a.a1 : 2.0 * a.a1);
+  a.C2f = (float)(2.0 * sar::kPi * (bistatic ? a.c2 : 2.0 * a.c2));
+  cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
+  plan->launches.fetch_add(1);
+  return SAR_OK;
+}
+
+sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,
+                            const double* tx_host, const double* rx_host,
+                            const float* doppler_host, sar_complex64_t* image_host,
+                            sar_stream_t stream) {
+  if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
+  const sar_radar_params_t& r = plan->radar;
+  const sar_grid_t& g = plan->grid;
+  if (!raw_host || !tx_host || !image_host)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "raw_host, tx_host and image_host must be non-null");
+  if (!rx_host && r.n_rx != 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "rx_host may be NULL only when n_rx == 1");
+  // Coverage check of the declared antenna box (the crop relies on it).
+  const double tol = 1e-9;
+  auto inside = [&](const double* q) {
+    for (int k = 0; k < 3; ++k)
+      if (!(q[k] >= plan->box.lo[k] - tol && q[k] <= plan->box.hi[k] + tol)) return false;
+    return true;
+  };
+  for (int m = 0; m < r.n_chirps; ++m) {
+    if (!inside(tx_host + 3 * (size_t)m))
+      return fail(SAR_ERR_OUT_OF_COVERAGE, "a TX position lies outside the declared antenna box");
+    if (rx_host)
+      for (int n = 0; n < r.n_rx; ++n)
+        if (!inside(rx_host + 3 * ((size_t)m * r.n_rx + n)))
+          return fail(SAR_ERR_OUT_OF_COVERAGE, "an RX position lies outside the declared antenna box");
+  }
+  DeviceGuard guard(plan->device);
+  const size_t M = r.n_chirps, R = r.n_rx, NS = r.n_samples, NB = plan->info.n_bins;
+  const size_t npix = (size_t)g.nx * g.ny;
+  sar_status_t st;
+  if (!plan->w_raw) {
+    if ((st = dev_alloc(&plan->w_raw, M * R * NS)) != SAR_OK || (st = dev_alloc(&plan->w_wsar, M)) != SAR_OK ||
+        (st = dev_alloc(&plan->w_tx, M * 3)) != SAR_OK || (st = dev_alloc(&plan->w_rx, M * R * 3)) != SAR_OK ||
+        (st = dev_alloc(&plan->w_dop, npix)) != SAR_OK || (st = dev_alloc(&plan->w_prof, M * R * NB)) != SAR_OK ||
+        (st = dev_alloc(&plan->w_img, npix)) != SAR_OK)
+      return st;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(plan->w_raw, raw_host, M * R * NS * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(plan->w_tx, tx_host, M * 3 * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync H2D");
+  if (w_sar_host && (e = cudaMemcpyAsync(plan->w_wsar, w_sar_host, M * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync H2D");
+  if (rx_host && (e = cudaMemcpyAsync(plan->w_rx, rx_host, M * R * 3 * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync H2D");
+  if (doppler_host && (e = cudaMemcpyAsync(plan->w_dop, doppler_host, npix * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync H2D");
+  st = sar_range_compress(plan, plan->w_raw, w_sar_host ? plan->w_wsar : nullptr, 0, r.n_chirps,
+                          reinterpret_cast<sar_complex64_t*>(plan->w_prof), stream);
+  if (st != SAR_OK) return st;
+  st = sar_backproject(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
+                       rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0,
+                       r.n_chirps, 0, g.ny, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, stream);
+  if (st != SAR_OK) return st;
+  if ((e = cudaMemcpyAsync(image_host, plan->w_img, npix * sizeof(float2), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync D2H");
+  return SAR_OK;
+}
+
+sar_status_t sar_destroy(sar_plan_t plan) {
+  if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
+  DeviceGuard guard(plan->device);
+  free_plan(plan);
+  return SAR_OK;
+}
+
+}  // extern "C"

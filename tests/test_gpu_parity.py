@@ -1,0 +1,276 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the fp64 oracle on the same
+seeded inputs.  Bar (north star): peak pixel indices equal and
+max|img_gpu - img_ref| / max|img_ref| <= 1e-3; profiles within 1e-5 of max|ref|."""
+import numpy as np
+import pytest
+
+import oracle
+import sarsim
+from sarsim import C_LIGHT, Grid, Scenario
+
+from .helpers import REL_TOL, gpu_image, oracle_image, oracle_profiles, rel_err, sample_indices
+
+pytestmark = pytest.mark.gpu
+
+
+def _raw(scn):
+    import torch
+
+    return sarsim.simulate_raw(scn, device="cuda:0")
+
+
+# ----------------------------------------------------------------------------- range compression
+@pytest.mark.parametrize("cfg", ["C1", "small_hann", "small_rect_odd", "C2_256"])
+def test_rc_profiles_match_oracle(cuda_lib, cfg):
+    if cfg == "C1":
+        scn = sarsim.make_config("C1", wsar="hann")
+    elif cfg == "small_hann":
+        scn = sarsim.small_config(n_chirps=37, ns=128, n_rx=3, seed=5, noise_sigma=0.1)
+        scn.wsar = np.linspace(0.2, 1.0, 37).astype(np.float32)
+    elif cfg == "small_rect_odd":
+        scn = sarsim.small_config(n_chirps=5, ns=64, seed=6)
+        scn.radar = sarsim.Radar(n_samples=64, fft_len=2048, range_window=0)   # Z = 32, odd log2
+    else:
+        scn = sarsim.make_config("C2", n_chirps=256)
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    ref = oracle_profiles(scn, raw.cpu().numpy(), plan.k_lo, plan.n_bins)
+    got = prof.cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    plan.close()
+    assert err < 1e-5, err
+
+
+def test_rc_chirp_shards_write_only_their_rows(cuda_lib):
+    import torch
+
+    scn = sarsim.small_config(n_chirps=20, ns=128, n_rx=2, seed=8)
+    raw = _raw(scn)
+    lo, hi = scn.antenna_box(1e-3)
+    plan = cuda_lib.Plan(scn.radar, scn.grid, 20, 2, (lo, hi))
+    full = plan.range_compress(raw)
+    part = torch.full_like(full, complex(7.0, 7.0))
+    plan.range_compress(raw, chirp0=5, nchirp=9, out=part)
+    torch.cuda.synchronize()
+    assert torch.equal(part[5:14], full[5:14])
+    assert torch.all(part[:5] == complex(7.0, 7.0)) and torch.all(part[14:] == complex(7.0, 7.0))
+    plan.close()
+
+
+# ----------------------------------------------------------------------------- full chain, small
+def test_C1_full_image_parity(cuda_lib):
+    scn = sarsim.make_config("C1")
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref)) == 32 * 64 + 32
+    assert rel_err(got, ref) <= REL_TOL
+    # phase at the peak: arg P(p*) = arg a (A2) to 1e-3 rad
+    assert abs(np.angle(got[32 * 64 + 32])) < 1e-3
+
+
+@pytest.mark.parametrize("kind", ["ragged_straight", "curved_bistatic", "curved_hann", "fine_grid"])
+def test_small_scenes_full_image_parity(cuda_lib, kind):
+    if kind == "ragged_straight":
+        scn = sarsim.small_config(n_chirps=96, ns=256, nx=77, ny=45, seed=21)
+    elif kind == "curved_bistatic":
+        scn = sarsim.small_config(n_chirps=64, ns=256, nx=50, ny=33, n_rx=3, curved=True, seed=22)
+    elif kind == "curved_hann":
+        scn = sarsim.small_config(n_chirps=128, ns=256, nx=64, ny=64, curved=True, seed=23, noise_sigma=0.2)
+        u = np.arange(128) / 127.0
+        scn.wsar = (0.5 - 0.5 * np.cos(2 * np.pi * u)).astype(np.float32)
+    else:
+        scn = sarsim.small_config(n_chirps=64, ns=256, nx=70, ny=40, seed=24, grid_dx=0.004)
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    assert rel_err(got, ref) <= REL_TOL
+    for (j, i) in scn.isolated:
+        w = np.abs(got.reshape(scn.grid.ny, scn.grid.nx))
+        assert w[j, i] == w[max(0, j - 2):j + 3, max(0, i - 2):i + 3].max()
+
+
+# ----------------------------------------------------------------------------- closed forms on GPU
+def test_flat_profile_exact_coherent_sum_gpu(cuda_lib):
+    """T4 on the GPU BP alone: X_m[k] = a exp(-j 2 pi f0 d_m(p*)/c) for all k -> P(p*) = a M."""
+    import torch
+
+    r = sarsim.Radar(n_samples=256, fft_len=2048)
+    M = 300
+    tx = sarsim.curved_track(M, r.pri_s, 6, 9, 20.0)
+    grid = Grid(-0.5, 20.0, 0.0, 0.01, 0.01, 64, 40)
+    pj, pi_ = 17, 41
+    p = np.array([grid.x0 + pi_ * grid.dx, grid.y0 + pj * grid.dy, 0.0])
+    d = 2 * np.linalg.norm(tx - p, axis=1)
+    a = 0.8 * np.exp(0.3j)
+    lo, hi = tx.min(0) - 1e-3, tx.max(0) + 1e-3
+    plan = cuda_lib.Plan(r, grid, M, 1, (lo, hi))
+    row = a * np.exp(-2j * np.pi * r.f0_hz * d / C_LIGHT)
+    prof = torch.as_tensor(np.repeat(row[:, None, None], plan.n_bins, axis=2).astype(np.complex64), device="cuda:0")
+    img = plan.backproject(prof, torch.as_tensor(tx, device="cuda:0"))
+    torch.cuda.synchronize()
+    v = complex(img[pj, pi_].item())
+    plan.close()
+    # the only error left is fp32 rounding of the flat row itself (1e-7) and the range form
+    assert abs(v - a * M) < 1e-5 * M, (v, a * M)
+
+
+def test_translation_invariance_gpu(cuda_lib):
+    """T7: a 1 km shift of track, grid and scene changes nothing (fp32 accuracy form)."""
+    scn = sarsim.small_config(n_chirps=128, ns=256, nx=48, ny=40, seed=31)
+    raw = _raw(scn)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    sh = np.array([1000.0, 1000.0, 0.0])
+    g = scn.grid
+    scn2 = Scenario("shift", scn.radar, Grid(g.x0 + 1000, g.y0 + 1000, 0.0, g.dx, g.dy, g.nx, g.ny),
+                    scn.tx + sh, None, scn.targets + sh, scn.amps, scn.isolated, scn.wsar)
+    got = gpu_image(scn2, raw).cpu().numpy().reshape(-1)
+    assert rel_err(got, ref) <= REL_TOL
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+
+
+def test_chirp_permutation_gpu(cuda_lib):
+    scn = sarsim.small_config(n_chirps=96, ns=256, nx=40, ny=30, curved=True, n_rx=2, seed=32)
+    raw = _raw(scn)
+    a = gpu_image(scn, raw).cpu().numpy()
+    perm = np.random.default_rng(2).permutation(96)
+    scn2 = Scenario("perm", scn.radar, scn.grid, scn.tx[perm], scn.rx[perm], scn.targets, scn.amps,
+                    scn.isolated, scn.wsar[perm])
+    b = gpu_image(scn2, raw[perm.tolist()].contiguous()).cpu().numpy()
+    assert rel_err(b, a) < 1e-5
+
+
+def test_doppler_term_matches_oracle(cuda_lib):
+    """Alg. 2 L8 f_doppler(p) (Measure D): per-pixel index shift, same on both sides."""
+    scn = sarsim.small_config(n_chirps=64, ns=256, nx=40, ny=36, seed=33)
+    g = scn.grid
+    rng = np.random.default_rng(0)
+    dop = rng.uniform(-0.6, 0.6, (g.ny, g.nx)).astype(np.float32)
+    raw = _raw(scn)
+    got = gpu_image(scn, raw, doppler=dop, dop_max=0.6).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy(), doppler=dop.reshape(-1).astype(np.float64))
+    assert rel_err(got, ref) <= REL_TOL
+
+
+def test_near_field_pixel_on_antenna(cuda_lib):
+    """T9: a pixel coincident with an antenna phase centre stays finite and matches the oracle."""
+    r = sarsim.Radar(n_samples=256, fft_len=2048)
+    M = 32
+    tx = sarsim.straight_track(M, r.wavelength_m / 4, y=1.0)
+    grid = Grid(-0.3, 0.9, 0.0, 0.01, 0.01, 64, 48)      # contains the track
+    tx[:, 0] = np.round((tx[:, 0] - grid.x0) / 0.01) * 0.01 + grid.x0  # antennas on pixel centres
+    scn = Scenario("near", r, grid, tx, None, np.array([[0.05, 1.2, 0.0]]), np.array([1.0 + 0j]),
+                   np.zeros((0, 2), int), np.ones(M, np.float32))
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    assert np.all(np.isfinite(got))
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert rel_err(got, ref) <= REL_TOL
+
+
+# ----------------------------------------------------------------------------- shards and edges
+def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
+    import torch
+
+    scn = sarsim.small_config(n_chirps=100, ns=256, nx=70, ny=90, seed=41, n_rx=2)
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    rx = torch.as_tensor(scn.rx, device="cuda:0").contiguous()
+    rows = torch.cat([plan.backproject(prof, tx, rx, row0=r0, nrow=n) for r0, n in ((0, 23), (23, 40), (63, 27))])
+    acc = plan.backproject(prof, tx, rx, chirp0=0, nchirp=37)
+    plan.backproject(prof, tx, rx, chirp0=37, nchirp=63, out=acc, accumulate=True)
+    torch.cuda.synchronize()
+    a = img.cpu().numpy()
+    assert rel_err(rows.cpu().numpy(), a) < 1e-5
+    assert rel_err(acc.cpu().numpy(), a) < 1e-5
+    # empty chirp shard: zeros (overwrite) / untouched (accumulate); empty row shard: no-op
+    z = plan.backproject(prof, tx, rx, chirp0=10, nchirp=0)
+    keep = acc.clone()
+    plan.backproject(prof, tx, rx, chirp0=10, nchirp=0, out=acc, accumulate=True)
+    plan.backproject(prof, tx, rx, row0=5, nrow=0, out=acc[:0])
+    torch.cuda.synchronize()
+    assert torch.all(z == 0) and torch.equal(acc, keep)
+    plan.close()
+
+
+def test_one_pixel_grid_and_single_chirp(cuda_lib):
+    scn = sarsim.small_config(n_chirps=1, ns=128, nx=1, ny=1, seed=42)
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert abs(got[0] - ref[0]) <= REL_TOL * max(abs(ref[0]), 1e-30) + 1e-6
+
+
+def test_error_codes(cuda_lib):
+    import torch
+
+    sar = cuda_lib
+    scn = sarsim.small_config(n_chirps=8, ns=64, nx=16, ny=16, seed=43)
+    lo, hi = scn.antenna_box(1e-3)
+    plan = sar.Plan(scn.radar, scn.grid, 8, 1, (lo, hi))
+    raw = _raw(scn)
+    prof = plan.range_compress(raw)
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    with pytest.raises(sar.SarError) as e:
+        plan.backproject(prof, tx, chirp0=4, nchirp=5)
+    assert e.value.status == 1
+    with pytest.raises(sar.SarError):
+        plan.backproject(prof, tx, row0=10, nrow=7)
+    with pytest.raises(sar.SarError):
+        sar.sar_backproject(plan.handle, prof.data_ptr(), None, None, None, 0, 8, 0, 16, prof.data_ptr())
+    with pytest.raises(sar.SarError):   # Doppler array without a declared bound
+        plan.backproject(prof, tx, doppler=torch.zeros((16, 16), device="cuda:0"))
+    # coverage: a TX position outside the declared box
+    bad = scn.tx.copy()
+    bad[3, 1] += 5.0
+    with pytest.raises(sar.SarError) as e:
+        plan.form_image(raw.cpu().contiguous(), torch.as_tensor(bad))
+    assert e.value.status == 2
+    plan.close()
+
+
+def test_form_image_host_buffers_equal_device_path(cuda_lib):
+    import torch
+
+    scn = sarsim.small_config(n_chirps=64, ns=256, nx=40, ny=33, seed=44, n_rx=2)
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    raw_h = raw.cpu().pin_memory()
+    out = plan.form_image(raw_h, torch.as_tensor(scn.tx).pin_memory(), torch.as_tensor(scn.rx).contiguous(),
+                          torch.as_tensor(scn.wsar))
+    torch.cuda.synchronize()
+    assert torch.equal(out, img.cpu())
+    assert plan.launches >= 4
+    plan.close()
+
+
+# ----------------------------------------------------------------------------- full-size configs
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4"])
+def test_full_size_config_sampled_parity(cuda_lib, cfg):
+    """BASELINE configs at full size in the bench's launch configuration; the oracle on the
+    C-6 sample (strided rows/cols + windows around isolated targets and GPU maxima)."""
+    scn = sarsim.make_config(cfg)
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    a = np.abs(img.cpu().numpy())
+    g = scn.grid
+    stride = {"C2": (97, 101), "C3": (149, 151), "C0": (61, 67), "C4": (397, 401)}[cfg]
+    idx = sample_indices(scn, a, stride=stride, win=2 if cfg == "C4" else 3)
+    pix = g.pixel_list(idx)
+    # oracle on the crop the plan keeps (it raises if any pixel needed a bin outside it)
+    ref_prof = oracle_profiles(scn, raw.cpu().numpy(), plan.k_lo, plan.n_bins)
+    ref = oracle.backproject(ref_prof, plan.k_lo, scn.radar, scn.tx, scn.rx, pix)
+    got = img.cpu().numpy()[idx[:, 0], idx[:, 1]]
+    plan.close()
+    assert rel_err(got, ref) <= REL_TOL
+    # global peak: the pole (a = 1) on both sides
+    pole = tuple(scn.isolated[0])
+    assert np.unravel_index(np.argmax(a), a.shape) == pole
+    k = np.argmax(np.abs(ref))
+    assert tuple(idx[k]) == pole
+    # local argmax of every isolated target agrees (within its sampled window)
+    for (j, i) in scn.isolated:
+        sel = (np.abs(idx[:, 0] - j) <= 2) & (np.abs(idx[:, 1] - i) <= 2)
+        assert np.argmax(np.abs(got[sel])) == np.argmax(np.abs(ref[sel]))
