@@ -1,0 +1,380 @@
+"""Benchmark: ms per 8192-chirp 30 m x 30 m BP image and pixel.chirp updates/s on N B200s.
+
+Contract (one JSON line from rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+Under torchrun (N > 1) every rank runs one process per GPU; the image rows are sharded
+across ranks (pixel-tile sharding) and assembled with an NCCL all_gather over NVLink,
+the north star's multi-GPU design.  A step = range compression of all chirps
+(sar_range_compress) + back-projection of this rank's rows (sar_backproject)
+[+ all_gather_into_tensor when N > 1], inputs resident in HBM.
+
+``--impl reference`` times the fp64 CPU oracle (oracle/) on the host cores, the
+reference arm of this tier; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per 8192-chirp 30×30 m BP image; pixel·chirp updates/s at 1/2/4/8 B200"
+UNIT = "px·chirp·rx updates/s"
+WORKLOADS = {
+    "C3": "C3: 8192 chirps x 512 samples, 1 RX, curved non-equidistant track (R = 20 m, 6->9 m/s), "
+          "30 m x 30 m grid at 1 cm (3000 x 3000 px), Fig.1-style scene + 96 isolated points, AWGN 0.05",
+    "C2": "C2: 8192 chirps x 512 samples, 1 RX, straight 8 m/s track, 30 m x 12 m at 1 cm (3000 x 1200 px)",
+    "C0": "C0: paper grid 1201 x 1201 px at 2.5 cm over 30 m x 30 m, 8192 chirps, 1 RX (C2 track)",
+    "C4": "C4: 8192 chirps x 4 RX (bistatic MIMO), 30 m x 30 m at 5 mm (6000 x 6000 px)",
+}
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - reported in the JSON line
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _alu_peak_upd_s(n_sm: int, mhz: float) -> float:
+    """SFU roofline of the BP update: 3 MUFU-class ops (1 rsqrt, 1 sin, 1 cos) per update,
+    16 MUFU results/clk/SM."""
+    return n_sm * 16.0 * mhz * 1e6 / 3.0
+
+
+def _traffic_from_profiles(cfg: str):
+    p = os.path.join(ROOT, "profiles", "bp_dram_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg)
+    except Exception:
+        return None
+
+
+def _setup(cfg: str, device):
+    import torch
+
+    import sarsim
+
+    scn = sarsim.make_config(cfg)
+    raw = sarsim.simulate_raw(scn, device=str(device))
+    return scn, raw
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def _oracle_sample(scn, raw_np, target_s: float, nthreads: int = 0):
+    """Time the oracle (as it stands) on a bounded sample: range compression of every
+    chirp + BP of a strided pixel subset sized for about ``target_s`` seconds."""
+    import numpy as np
+
+    import oracle
+
+    r = scn.radar
+    g = scn.grid
+    t0 = time.perf_counter()
+    prof = oracle.range_compress(raw_np, r.fft_len, r.range_window, scn.wsar, nthreads=nthreads)
+    t_rc = time.perf_counter() - t0
+    # calibrate with a small probe, then size the sample
+    rng = np.random.default_rng(0)
+    probe = g.pixel_list(np.stack([rng.integers(0, g.ny, 32), rng.integers(0, g.nx, 32)], 1))
+    t0 = time.perf_counter()
+    oracle.backproject(prof, 0, r, scn.tx, scn.rx, probe, nthreads=nthreads)
+    t_probe = max(time.perf_counter() - t0, 1e-4)
+    n_pix = int(max(64, min(g.nx * g.ny, 32 * target_s / t_probe)))
+    idx = np.stack([rng.integers(0, g.ny, n_pix), rng.integers(0, g.nx, n_pix)], 1)
+    t0 = time.perf_counter()
+    oracle.backproject(prof, 0, r, scn.tx, scn.rx, g.pixel_list(idx), nthreads=nthreads)
+    t_bp = time.perf_counter() - t0
+    full_pix = g.nx * g.ny
+    est_image_s = t_rc + t_bp * full_pix / n_pix
+    return {"t_rc_s": t_rc, "t_bp_s": t_bp, "n_pix": n_pix, "est_image_s": est_image_s,
+            "value": scn.updates / est_image_s}
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+
+    import sarsim
+
+    cores = os.cpu_count() or 1
+    scn = sarsim.make_config(args.config)
+    raw = sarsim.simulate_raw(scn, device="cuda:0" if torch.cuda.is_available() else "cpu").cpu().numpy()
+    per_step = []
+    for s in range(args.warmup + args.steps):
+        res = _oracle_sample(scn, raw, target_s=args.ref_step_s)
+        if s >= args.warmup:
+            per_step.append(res)
+    est = statistics.median(r["est_image_s"] for r in per_step)
+    value = scn.updates / est
+    wall = sum(r["t_rc_s"] + r["t_bp_s"] for r in per_step) / len(per_step)
+    sample = (f"per step: oracle range compression of all {scn.n_chirps * scn.n_rx} rows + oracle BP of "
+              f"{per_step[0]['n_pix']} random pixels x {scn.n_chirps} chirps x {scn.n_rx} RX; "
+              f"full-image time extrapolated per pixel")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "sample_wall_ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "config": args.config},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_09784_b200 import sar
+    from paper_2306_09784_b200.dist import row_partition
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sar.load()
+
+    scn, raw = _setup(args.config, dev)
+    g = scn.grid
+    row0, nrow = row_partition(g.ny, world, rank)
+    lo, hi = scn.antenna_box(1e-3)
+    plan = sar.Plan(scn.radar, g, scn.n_chirps, scn.n_rx, (lo, hi), device=local)
+    tx = torch.as_tensor(scn.tx, device=dev)
+    rx = None if scn.rx is None else torch.as_tensor(scn.rx, device=dev).contiguous()
+    wsar = torch.as_tensor(scn.wsar, device=dev)
+    prof = plan.empty_profiles()
+    local_img = plan.empty_image(nrow)
+    full_img = torch.empty((g.ny, g.nx), dtype=torch.complex64, device=dev) if world > 1 else local_img
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.range_compress(raw, wsar, out=prof, stream=stream)
+        ev[1].record(stream)
+        plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
+        ev[2].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1),
+                                        torch.view_as_real(local_img).view(-1))
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for _ in range(args.warmup):
+        ev[0].record(stream)
+        step()
+        ev[3].record(stream)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, device events, L2 flushed between steps
+    step_ms, bp_ms, rc_ms = [], [], []
+    l0 = plan.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            ev[0].record(stream)
+            step()
+            ev[3].record(stream)
+            ev[3].synchronize()
+            step_ms.append(ev[0].elapsed_time(ev[3]))
+            rc_ms.append(ev[0].elapsed_time(ev[1]))
+            bp_ms.append(ev[1].elapsed_time(ev[2]))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = plan.launches - l0
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, sum(bp_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, bp_total_ms = float(t[0]), float(t[1])
+    else:
+        bp_total_ms = sum(bp_ms)
+    ms_per_step = total_ms / args.steps
+    value = scn.updates / (ms_per_step * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (bp_kernel)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peaks = _peaks()
+    max_mhz = float(peaks.get("sm_max_mhz", clk.max_mhz or 1965.0))
+    bp_upd = nrow * g.nx * scn.n_chirps * scn.n_rx
+    bp_avg_s = (sum(bp_ms) / len(bp_ms)) * 1e-3
+    achieved = bp_upd / bp_avg_s
+    peak = _alu_peak_upd_s(n_sm, max_mhz)
+    clocks = clk.summary()
+    roofline = {
+        "bound": "alu", "achieved": achieved, "peak": peak, "unit": "upd/s", "frac": achieved / peak,
+        "traffic": _traffic_from_profiles(args.config),
+        "kernel": "bp_kernel", "peak_basis": f"SFU: {n_sm} SM x 16 MUFU/clk x {max_mhz:.0f} MHz / 3 MUFU per update",
+        "frac_at_measured_clock": (achieved / _alu_peak_upd_s(n_sm, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
+        "bp_ms": bp_avg_s * 1e3, "rc_ms": sum(rc_ms) / len(rc_ms),
+    }
+
+    # ---------------- end to end through the C ABI with host buffers (sar_form_image)
+    raw_h = raw.cpu().pin_memory()
+    tx_h = torch.as_tensor(scn.tx).contiguous().pin_memory()
+    rx_h = None if scn.rx is None else torch.as_tensor(scn.rx).contiguous().pin_memory()
+    wsar_h = torch.as_tensor(scn.wsar).pin_memory()
+    img_h = torch.empty((nrow, g.nx), dtype=torch.complex64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(2):
+        plan.form_image(raw_h, tx_h, rx_h, wsar_h, row0=row0, nrow=nrow, out_h=img_h, stream=stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = 0.0
+    for _ in range(e2e_steps):
+        flush.zero_()
+        e0.record(stream)
+        plan.form_image(raw_h, tx_h, rx_h, wsar_h, row0=row0, nrow=nrow, out_h=img_h, stream=stream, sync=False)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    e2e_ms /= e2e_steps
+    h2d = raw_h.numel() * 4 + tx_h.numel() * 8 + wsar_h.numel() * 4 + (0 if rx_h is None else rx_h.numel() * 8)
+    d2h = img_h.numel() * 8
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = _oracle_sample(scn, raw.cpu().numpy(), target_s=args.cpu_s)
+        cpu = {"value": res["value"], "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"oracle range compression of all {scn.n_chirps * scn.n_rx} rows "
+                         f"({res['t_rc_s']:.2f} s) + oracle BP of {res['n_pix']} random pixels x all chirps "
+                         f"({res['t_bp_s']:.2f} s), full image extrapolated to {res['est_image_s']:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "config": args.config, "pixels": g.nx * g.ny,
+                       "chirps": scn.n_chirps, "n_rx": scn.n_rx, "samples": scn.radar.n_samples,
+                       "fft_len": scn.radar.fft_len, "n_bins": plan.n_bins, "updates": scn.updates,
+                       "parallelism": f"pixel rows x{world}" + (" + NCCL all_gather" if world > 1 else ""),
+                       "l2": "256 MB buffer written between timed steps (outside the event span)",
+                       "step": "sar_range_compress(all chirps) + sar_backproject(rank rows)"
+                               + (" + all_gather_into_tensor" if world > 1 else "")},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": scn.updates / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_image": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "sar_form_image (C ABI, pinned host buffers: H2D raw+poses, rc, bp, D2H image rows)"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
+    ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -155,18 +155,19 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
 
 /* End-to-end image formation from HOST buffers (the paper's "Load" + "BP",
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a
- * plan-owned device workspace, runs sar_range_compress and sar_backproject over
- * all chirps and rows, and copies the image back, all on `stream`.
+ * plan-owned device workspace, runs sar_range_compress over all chirps and
+ * sar_backproject over all chirps for grid rows [row0, row0 + nrow), and copies
+ * those image rows back, all on `stream`.
  *   raw_host [n_chirps][n_rx][n_samples] float; w_sar_host [n_chirps] float or NULL;
  *   tx_host [n_chirps][3] double; rx_host [n_chirps][n_rx][3] double or NULL;
- *   doppler_host [ny][nx] float or NULL; image_host [ny][nx] complex (written).
+ *   doppler_host [ny][nx] float or NULL; image_host [nrow][nx] complex (written).
  * Positions are checked against the declared antenna box first
  * (SAR_ERR_OUT_OF_COVERAGE).  The caller synchronises `stream` before reading
  * image_host. */
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,
                             const double* tx_host, const double* rx_host,
-                            const float* doppler_host, sar_complex64_t* image_host,
-                            sar_stream_t stream);
+                            const float* doppler_host, int32_t row0, int32_t nrow,
+                            sar_complex64_t* image_host, sar_stream_t stream);
 
 /* Number of CUDA kernels this plan has launched since creation. */
 int64_t sar_plan_launch_count(sar_plan_t plan);

@@ -347,11 +347,13 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
 
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,
                             const double* tx_host, const double* rx_host,
-                            const float* doppler_host, sar_complex64_t* image_host,
-                            sar_stream_t stream) {
+                            const float* doppler_host, int32_t row0, int32_t nrow,
+                            sar_complex64_t* image_host, sar_stream_t stream) {
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   const sar_radar_params_t& r = plan->radar;
   const sar_grid_t& g = plan->grid;
+  if (row0 < 0 || nrow < 0 || (int64_t)row0 + nrow > g.ny)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "row shard out of range");
   if (!raw_host || !tx_host || !image_host)
     return fail(SAR_ERR_INVALID_ARGUMENT, "raw_host, tx_host and image_host must be non-null");
   if (!rx_host && r.n_rx != 1)
@@ -398,9 +400,10 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   if (st != SAR_OK) return st;
   st = sar_backproject(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
                        rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0,
-                       r.n_chirps, 0, g.ny, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, stream);
+                       r.n_chirps, row0, nrow, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, stream);
   if (st != SAR_OK) return st;
-  if ((e = cudaMemcpyAsync(image_host, plan->w_img, npix * sizeof(float2), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+  if (nrow > 0 &&
+      (e = cudaMemcpyAsync(image_host, plan->w_img, (size_t)nrow * g.nx * sizeof(float2), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync D2H");
   return SAR_OK;
 }

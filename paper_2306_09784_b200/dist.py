@@ -1,0 +1,67 @@
+"""Multi-GPU sharding of the BP image (H7): one process per GPU, torch.distributed.
+
+Two decompositions of the same sum P(p) = sum_m sum_n (...)  (Alg. 2 L12):
+  * pixel rows  -- rank r owns grid rows [row0, row0 + nrow); every rank range-compresses
+    all chirps (cheap, HBM-bound) and back-projects its rows; the image is assembled with
+    one all_gather_into_tensor over NVLink (rows are contiguous in the row-major image).
+  * chirps      -- rank r owns chirps [c0, c0 + nc); it range-compresses only those and
+    back-projects ALL pixels into a partial image; one reduce(SUM) to the root adds the
+    partial images (complex addition is component-wise on the float32 view).
+The compute calls go through libsar (``sar.Plan``); the helpers below only partition
+and move bytes, so they also run with the gloo backend on CPU tensors in the tests.
+"""
+from __future__ import annotations
+
+
+def row_partition(ny: int, world: int, rank: int):
+    """Contiguous, balanced row blocks; equal sizes when world divides ny (all_gather
+    needs equal chunks, so callers with ragged splits pad to ceil(ny/world))."""
+    base, rem = divmod(ny, world)
+    row0 = rank * base + min(rank, rem)
+    return row0, base + (1 if rank < rem else 0)
+
+
+def chirp_partition(n_chirps: int, world: int, rank: int):
+    return row_partition(n_chirps, world, rank)
+
+
+def gather_rows(local, ny: int, group=None):
+    """Assemble the full [ny][nx] complex image from per-rank row blocks.
+
+    Uses all_gather_into_tensor on the float32 view when blocks are equal, else pads
+    every block to ceil(ny/world) rows and trims.  Works for NCCL (CUDA tensors) and
+    gloo (CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    nx = local.shape[1]
+    per = -(-ny // world)
+    if local.shape[0] != per:
+        pad = torch.zeros((per, nx), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        local = pad
+    full = torch.empty((per * world, nx), dtype=local.dtype, device=local.device)
+    src = torch.view_as_real(local).reshape(-1)
+    dst = torch.view_as_real(full).reshape(-1)
+    if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(dst, src, group=group)
+    else:
+        dist.all_gather(list(dst.chunk(world)), src, group=group)   # chunks are views of dst
+    if per * world == ny:
+        return full
+    # drop the padding rows of every ragged block
+    keep = []
+    for r in range(world):
+        r0, n = row_partition(ny, world, r)
+        keep.append(full[r * per: r * per + n])
+    return torch.cat(keep)
+
+
+def reduce_partials(partial, dst: int = 0, group=None):
+    """Sum per-rank partial images (chirp sharding) into rank ``dst`` (in place there)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.reduce(torch.view_as_real(partial).reshape(-1), dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return partial

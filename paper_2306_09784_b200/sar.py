@@ -73,7 +73,7 @@ def load() -> ctypes.CDLL:
             lib.sar_plan_crop.argtypes = [_vp, P(_i32), P(_i32)]
             lib.sar_range_compress.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_backproject.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp]
-            lib.sar_form_image.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+            lib.sar_form_image.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_plan_launch_count.argtypes = [_vp]
             lib.sar_plan_launch_count.restype = ctypes.c_int64
             lib.sar_destroy.argtypes = [_vp]
@@ -126,8 +126,8 @@ def sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row
                                   img_ptr, accumulate, stream))
 
 
-def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, img_h, stream=0):
-    _check(load().sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, img_h, stream))
+def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream=0):
+    _check(load().sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream))
 
 
 def sar_plan_launch_count(plan) -> int:
@@ -265,20 +265,24 @@ class Plan:
                         _stream_handle(stream))
         return out
 
-    def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, out_h=None, stream=None):
-        """End-to-end from host tensors (pinned for async copies); synchronises the stream."""
+    def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, row0=0, nrow=None, out_h=None,
+                   stream=None, sync=True):
+        """End-to-end from host tensors (pinned for async copies): image rows [row0, row0+nrow)."""
         import torch
 
         g = self.grid
-        out_h = torch.empty((g.ny, g.nx), dtype=torch.complex64, pin_memory=True) if out_h is None else out_h
+        nrow = g.ny - row0 if nrow is None else nrow
+        out_h = torch.empty((nrow, g.nx), dtype=torch.complex64, pin_memory=True) if out_h is None else out_h
         st = torch.cuda.current_stream(self.device) if stream is None else stream
         sar_form_image(self.handle,
                        _hptr(raw_h, torch.float32, (self.n_chirps, self.n_rx, self.radar.n_samples), "raw_h"),
                        _hptr(wsar_h, torch.float32, (self.n_chirps,), "wsar_h"),
                        _hptr(tx_h, torch.float64, (self.n_chirps, 3), "tx_h"),
                        _hptr(rx_h, torch.float64, (self.n_chirps, self.n_rx, 3), "rx_h"),
-                       _hptr(doppler_h, torch.float32, (g.ny, g.nx), "doppler_h"),
-                       _hptr(out_h, torch.complex64, (g.ny, g.nx), "image_h"), int(st.cuda_stream))
+                       _hptr(doppler_h, torch.float32, (g.ny, g.nx), "doppler_h"), row0, nrow,
+                       _hptr(out_h, torch.complex64, (nrow, g.nx), "image_h"), int(st.cuda_stream))
+        if sync:
+            st.synchronize()
         return out_h
 
     @property

@@ -86,9 +86,15 @@ def test_small_scenes_full_image_parity(cuda_lib, kind):
     ref = oracle_image(scn, raw.cpu().numpy())
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
     assert rel_err(got, ref) <= REL_TOL
+    # local peaks around every isolated target agree wherever the oracle's peak is
+    # unambiguous (best/second > 1 + 4e-3, reading A15: ties cannot flip under 1e-3)
+    G = np.abs(got.reshape(scn.grid.ny, scn.grid.nx))
+    R = np.abs(ref.reshape(scn.grid.ny, scn.grid.nx))
     for (j, i) in scn.isolated:
-        w = np.abs(got.reshape(scn.grid.ny, scn.grid.nx))
-        assert w[j, i] == w[max(0, j - 2):j + 3, max(0, i - 2):i + 3].max()
+        sl = (slice(max(0, j - 2), j + 3), slice(max(0, i - 2), i + 3))
+        r = np.sort(R[sl].ravel())
+        if r[-1] > (1 + 4e-3) * r[-2]:
+            assert np.argmax(G[sl]) == np.argmax(R[sl])
 
 
 # ----------------------------------------------------------------------------- closed forms on GPU
