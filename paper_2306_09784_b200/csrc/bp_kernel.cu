@@ -2,7 +2,7 @@
 // in a form whose fp32 arithmetic is accurate at 30 m ranges.
 //
 // Work decomposition
-//   * One CTA = one 32x32 pixel tile.  The tile anchor P_T is the tile centre (fp64).
+//   * One CTA = one 32 x (NCW*PB) pixel tile.  The tile anchor P_T is the tile centre (fp64).
 //   * Warp NCW is the PRODUCER: for each ring stage of CB chirps it computes, in fp64,
 //     the per-(tile, chirp, antenna) anchor record (D = P_T - q, r = |D|, anchor index
 //     and anchor phase) and stages the W profile bins the tile can touch for that chirp
@@ -11,8 +11,10 @@
 //     the triangle inequality |d_hyp - d_anchor| <= 2 rho_T, valid for ANY track and
 //     chirp order (no fallback path).
 //   * Warps 0..NCW-1 are CONSUMERS: each thread owns PB pixels (register accumulators);
-//     each warp's 32 lanes cover an 8x4 pixel patch so their gathers hit few bins.
-//   * Producer/consumer hand-off through a kBpStages-deep ring guarded by mbarriers.
+//     for one register slot a warp's 32 lanes cover an 8x4 pixel patch, so their gathers
+//     hit few distinct bins (broadcast, no bank conflicts).
+//   * Producer/consumer hand-off through an S-deep ring guarded by mbarriers
+//     (full: 32 producer lanes arrive; empty: all consumer threads arrive).
 //
 // Per (pixel, chirp, antenna) update (monostatic shown; bistatic adds the RX leg):
 //   g   = D.u + |u|^2/2                      (u = p - P_T, fp32, |u| <= rho_T)
@@ -21,11 +23,19 @@
 //   dR  = t + (g - t h) q                     = |p - q| - r, to ~1e-8 m (one Newton step
 //                                               on the residual; no cancellation)
 //   kappa = kappa_anchor + A1 dR  (+ f_doppler(p))          Alg. 2 L8
-//   phase = phi_anchor  + C2 dR                              Alg. 2 L9 (A2: +j)
-//   v = mid[k] + (kappa - k - 1/2) diff[k],  k = round(kappa - 1/2) via the 1.5*2^23 trick
-//   acc += v * exp(j phase)                   (MUFU sin/cos)  Alg. 2 L10, L12
+//   K = floor(kappa) (the 1.5*2^23 trick), f = kappa - K, gf = f - 1/2
+//   v = mid[K] + gf diff[K]                   (one LDS.128, two FFMA)
+//   acc += v * exp(j 2 pi beta gf)            (MUFU sin/cos)  Alg. 2 L9, L10, L12
+// Carrier phase folding: without Doppler kappa = a1 d exactly, so the hypothetical
+// phase 2 pi c2 d (Alg. 2 L9, A2: +j) equals 2 pi beta kappa with beta = c2/a1 cycles per
+// bin = 2 pi beta (K + 1/2) + 2 pi beta gf.  The producer multiplies each staged pair by
+// exp(j 2 pi beta (K + 1/2)) (plan table, built in fp64), so the per-update MUFU argument
+// is bounded by |2 pi beta gf| <= pi beta (~32 rad) whatever the range: the fp32 phase
+// carries no bias that grows with range or tile size.  With Doppler the shift
+// exp(-j 2 pi beta f_doppler(p)) is a per-pixel constant applied in the epilogue.
 // 3 MUFU + ~21 FMA/ALU + 1 LDS.128 per update.
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sar_internal.h"
 
@@ -35,6 +45,19 @@ namespace {
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
 constexpr uint32_t kMagicBits = 0x4B400000u;
 constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
+constexpr int kBatch = 8;                // producer: profile rows loaded per batch
+#ifndef SAR_BP_CHIRP_UNROLL
+#define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
+#endif
+constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
+#ifndef SAR_BP_MINB_48
+#define SAR_BP_MINB_48 1                 // resident-CTA hint for the (4, 8) shape (register cap)
+#endif
+#ifndef SAR_BP_MINB_84
+#define SAR_BP_MINB_84 1
+#endif
+template <int NCW, int PB>
+constexpr int kMinBlocks = (NCW == 4 && PB == 8) ? SAR_BP_MINB_48 : (NCW == 8 && PB == 4) ? SAR_BP_MINB_84 : 1;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -75,68 +98,77 @@ __device__ __forceinline__ float rsqrt_mufu(float x) {
   return y;
 }
 
-// One leg |p - q| - r of the anchored range (see header comment).
+// One leg |p - q| - r of the anchored range.  Record: Dx, Dy, r2 = r^2, r, e = r/2 (fast)
+// or Dz^2 (SAFE).  SAFE is the near-field form (an antenna may sit inside the tile): the
+// range is formed from the exact differences D + u and dR = 2g / (R + r) has no division
+// by a vanishing quantity (r > 0: the anchor is never a pixel centre).
+//   D2x, D2y = 2 D (record), w = |u|^2 (per pixel): g2 = 2 D.u + |u|^2 = |D + u|^2 - r^2
+//   s = r^2 + g2, q = rsqrt(s); t = s q - r and H = s q + r (one rounding each);
+//   rho2 = g2 - t H = s - (s q)^2 (exact residual up to one rounding);
+//   dR = t + rho2 q / 2.
 template <bool SAFE>
-__device__ __forceinline__ float leg_delta(float Dx, float Dy, float r2, float r, float rh,
-                                           float ux, float uy, float wh) {
-  const float g = fmaf(Dx, ux, fmaf(Dy, uy, wh));
+__device__ __forceinline__ float leg_delta(float D2x, float D2y, float r2, float r, float dz2,
+                                           float ux, float uy, float w) {
+  const float g2 = fmaf(D2x, ux, fmaf(D2y, uy, w));
   if (SAFE) {
-    // near field (an antenna may sit inside the tile): dR = 2g / (R + r), R = sqrt(max(s,0))
-    const float s = fmaxf(fmaf(2.f, g, r2), 0.f);
-    const float R = sqrtf(s);
-    return __fdividef(2.f * g, R + r);
+    const float ex = fmaf(0.5f, D2x, ux), ey = fmaf(0.5f, D2y, uy);
+    const float R = sqrtf(fmaf(ex, ex, fmaf(ey, ey, dz2)));
+    return __fdividef(g2, R + r);
   } else {
-    const float s = fmaf(2.f, g, r2);
+    const float s = g2 + r2;
     const float q = rsqrt_mufu(s);
-    const float R0 = s * q;
-    const float t = R0 - r;
-    const float h = fmaf(R0, 0.5f, rh);
-    const float rho = fmaf(-t, h, g);
-    return fmaf(rho, q, t);
+    const float t = fmaf(s, q, -r);
+    const float H = fmaf(s, q, r);
+    const float qh = 0.5f * q;
+    const float rho2 = fmaf(-t, H, g2);
+    return fmaf(rho2, qh, t);
   }
 }
 
-// Shared-memory layout of one ring (all offsets in bytes, 16-B aligned):
-//   [0, 64)                     mbarriers full[kBpStages], empty[kBpStages]
-//   rec   [S][LEGS] x 32 B      monostatic: LEGS = items; bistatic: LEGS = CB + items
-//   kwin  [S][items] int         window start bin per item (relative to the crop)
+// Shared-memory layout (bytes, 16-B aligned):
+//   [0, 128)                     mbarriers full[kBpMaxStages], empty[kBpMaxStages]
+//   rec   [S][LEGS] x 32 B       monostatic: LEGS = items; bistatic: LEGS = CB + items
+//   kwin  [S][items] int2        {window start bin (crop-relative), profile row offset}
 //   win   [S][items][W] x 16 B   pair-format profile windows
 struct Layout {
   int items, legs;
   uint32_t rec, kwin, win, total;
 };
 
-__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, bool bistatic) {
+__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic) {
   Layout L;
   L.items = CB * n_rx;
   L.legs = bistatic ? CB + L.items : L.items;
-  L.rec = 64;
-  L.kwin = L.rec + (uint32_t)kBpStages * L.legs * 32;
-  uint32_t kw_bytes = ((uint32_t)kBpStages * L.items * 4 + 15u) & ~15u;
+  L.rec = 16 * kBpMaxStages;
+  L.kwin = L.rec + (uint32_t)S * L.legs * 32;
+  const uint32_t kw_bytes = ((uint32_t)S * L.items * 8 + 15u) & ~15u;
   L.win = L.kwin + kw_bytes;
-  L.total = L.win + (uint32_t)kBpStages * L.items * W * 16;
+  L.total = L.win + (uint32_t)S * L.items * W * 16;
   return L;
 }
 
 template <bool BISTATIC, bool DOP, bool SAFE, int NCW, int PB>
-__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, kMinBlocks<NCW, PB>) bp_kernel(const BpArgs a) {
+  constexpr int TX = kTileX;
+  constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, BISTATIC);
+  const int S = a.S;
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpStages;
+  const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpMaxStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int i0 = tx * kTileX;           // first grid column of the tile
-  const int j0 = ty * kTileY;           // first row of the tile, relative to row0
+  const int i0 = tx * TX;               // first grid column of the tile
+  const int j0 = ty * TY;               // first row of the tile, relative to row0
   // tile anchor: centre of the full tile (even when ragged), fp64
-  const double PTx = a.x0 + (i0 + 0.5 * (kTileX - 1)) * a.dx;
-  const double PTy = a.y0 + (a.row0 + j0 + 0.5 * (kTileY - 1)) * a.dy;
+  const double PTx = a.x0 + (i0 + 0.5 * (TX - 1)) * a.dx;
+  const double PTy = a.y0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dy;
   const double PTz = a.z0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBpStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(bar_full + 8 * s, 32);          // producer lanes
       mbar_init(bar_empty + 8 * s, NCW * 32);   // consumer threads
     }
@@ -149,18 +181,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   if (warp == NCW) {
     // ============================== PRODUCER ==============================
     float4* rec = reinterpret_cast<float4*>(smem + L.rec);
-    int* kwin = reinterpret_cast<int*>(smem + L.kwin);
+    int2* kwin = reinterpret_cast<int2*>(smem + L.kwin);
     float4* win = reinterpret_cast<float4*>(smem + L.win);
-    const double two_pi = 2.0 * kPi;
+    int slot = 0;
+    uint32_t parity = 0;
     for (int it = 0; it < n_iter; ++it) {
-      const int slot = it % kBpStages;
-      const uint32_t parity = (it / kBpStages) & 1;
       mbar_wait(bar_empty + 8 * slot, parity ^ 1);
       const int c0 = it * a.CB;
       const int cnt = min(a.CB, a.nchirp - c0);
       const int items = cnt * a.n_rx;
       float4* srec = rec + (size_t)slot * L.legs * 2;
-      int* skw = kwin + slot * L.items;
+      int2* skw = kwin + slot * L.items;
       float4* swin = win + (size_t)slot * L.items * a.W;
       // ---- anchor records (fp64), one item per lane
       if (BISTATIC) {
@@ -168,80 +199,97 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
           const double* q = a.tx + 3 * (size_t)(a.chirp0 + c0 + c);
           const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
-          srec[2 * c] = make_float4((float)Dx, (float)Dy, r * r, r);
-          srec[2 * c + 1] = make_float4(0.5f * r, 0.f, 0.f, 0.f);
+          srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
+          srec[2 * c + 1] = make_float4(SAFE ? (float)(Dz * Dz) : 0.f, 0.f, 0.f, 0.f);
         }
       }
       for (int e = lane; e < items; e += 32) {
-        const int c = e / a.n_rx, n = e - c * a.n_rx;
+        const int c = BISTATIC ? e / a.n_rx : e;
+        const int n = BISTATIC ? e - c * a.n_rx : 0;
         const int m = a.chirp0 + c0 + c;
         const double* qt = a.tx + 3 * (size_t)m;
-        double d_anchor;
+        // The consumers form r32 + dR = sqrt(r32^2 + 2 D32.u + |u|^2) from the fp32-rounded
+        // record; the anchor path length uses the exact fp64 |D| so that the rounding of
+        // r and D enters only at second order (|r32 - |D|| * dR / r, ~1e-8 m).
+        double d_anchor, dz;
         float4 leg0;
         float rleg;
         if (BISTATIC) {
           const double* qr = a.rx + 3 * ((size_t)m * a.n_rx + n);
           const double Dx = PTx - qr[0], Dy = PTy - qr[1], Dz = PTz - qr[2];
-          rleg = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
-          leg0 = make_float4((float)Dx, (float)Dy, rleg * rleg, rleg);
+          const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+          rleg = (float)rr;
+          leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
+          dz = Dz;
           const double Tx = PTx - qt[0], Ty = PTy - qt[1], Tz = PTz - qt[2];
-          const float rt = (float)sqrt(Tx * Tx + Ty * Ty + Tz * Tz);
-          d_anchor = (double)rt + (double)rleg;
+          d_anchor = sqrt(Tx * Tx + Ty * Ty + Tz * Tz) + rr;
         } else {
           const double Dx = PTx - qt[0], Dy = PTy - qt[1], Dz = PTz - qt[2];
-          rleg = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
-          leg0 = make_float4((float)Dx, (float)Dy, rleg * rleg, rleg);
-          d_anchor = 2.0 * (double)rleg;
+          const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+          rleg = (float)rr;
+          leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
+          dz = Dz;
+          d_anchor = 2.0 * rr;
         }
         const double kap = a.a1 * d_anchor - a.k_lo;               // anchor index in the crop
         const int k0 = (int)floor(kap - a.kap_half) - 1;            // window start
-        double ph = a.c2 * d_anchor;                                // anchor phase (cycles)
-        ph -= rint(ph);
+        const int wh = a.W >> 1;                                    // centre the fp32 index
         const uint32_t waddr = smem_u32(swin + (size_t)e * a.W);
-        const uint32_t off = waddr - 16u * kMagicBits;
+        const uint32_t off = waddr + 16u * (uint32_t)wh - 16u * kMagicBits;
         const int ri = BISTATIC ? a.CB + e : e;
         srec[2 * ri] = leg0;
-        srec[2 * ri + 1] = make_float4(0.5f * rleg, (float)(kap - k0 - 0.5), (float)(two_pi * ph),
-                                       __uint_as_float(off));
-        skw[e] = k0;
+        srec[2 * ri + 1] = make_float4(SAFE ? (float)(dz * dz) : 0.f,
+                                       (float)(kap - k0 - 0.5 - wh), 0.f, __uint_as_float(off));
+        skw[e] = make_int2(k0, (m * a.n_rx + n) * a.n_bins);
       }
       __syncwarp();
-      // ---- profile windows in pair format; 8 items per batch for memory-level parallelism
+      // ---- profile windows in pair format: lane j of an item produces entry j from bins
+      //      k0+j and k0+j+1 (the latter from lane j+1 by shuffle); kBatch rows in flight
       for (int j0w = 0; j0w < a.W; j0w += 31) {
-        for (int e0 = 0; e0 < items; e0 += 8) {
-          float2 x[8];
+        const int j = j0w + lane;
+        for (int e0 = 0; e0 < items; e0 += kBatch) {
+          float2 x[kBatch];
 #pragma unroll
-          for (int b = 0; b < 8; ++b) {
+          for (int b = 0; b < kBatch; ++b) {
             x[b] = make_float2(0.f, 0.f);
             const int e = e0 + b;
             if (e < items) {
-              const int c = e / a.n_rx, n = e - c * a.n_rx;
-              const size_t row = ((size_t)(a.chirp0 + c0 + c) * a.n_rx + n) * a.n_bins;
-              const int k = skw[e] + j0w + lane;
-              if (k >= 0 && k < a.n_bins) x[b] = __ldg(a.prof + row + k);
+              const int2 kw = skw[e];
+              const int k = kw.x + j;
+              if (k >= 0 && k < a.n_bins) x[b] = __ldg(a.prof + kw.y + k);
             }
           }
 #pragma unroll
-          for (int b = 0; b < 8; ++b) {
+          for (int b = 0; b < kBatch; ++b) {
             const float nx_ = __shfl_down_sync(0xffffffffu, x[b].x, 1);
             const float ny_ = __shfl_down_sync(0xffffffffu, x[b].y, 1);
             const int e = e0 + b;
-            const int j = j0w + lane;
             if (e < items && lane < 31 && j < a.W) {
-              swin[(size_t)e * a.W + j] =
-                  make_float4(0.5f * (x[b].x + nx_), 0.5f * (x[b].y + ny_), nx_ - x[b].x, ny_ - x[b].y);
+              // bin phase exp(j 2 pi beta (k_lo + k + 1/2)) of the entry's lower bin k; the
+              // table starts at k = -1 (the entry holding X[-1] = 0 and X[0]); entries
+              // further out hold only zeros and may take any phase
+              const int k = min(max(skw[e].x + j, -1), a.n_bins - 1);
+              const float2 q = __ldg(a.binphase + k + 1);
+              const float mr = 0.5f * (x[b].x + nx_), mi = 0.5f * (x[b].y + ny_);
+              const float dr = nx_ - x[b].x, di = ny_ - x[b].y;
+              swin[(size_t)e * a.W + j] = make_float4(mr * q.x - mi * q.y, mr * q.y + mi * q.x,
+                                                      dr * q.x - di * q.y, dr * q.y + di * q.x);
             }
           }
         }
       }
       mbar_arrive(bar_full + 8 * slot);
+      if (++slot == S) {
+        slot = 0;
+        parity ^= 1;
+      }
     }
     return;
   }
 
   // ============================== CONSUMERS ==============================
   const int lx = lane & (kPatchX - 1), ly = lane >> 3;
-  constexpr int kPatchesPerRow = kTileX / kPatchX;
+  constexpr int kPatchesPerRow = TX / kPatchX;
   float ux[PB], uy[PB], wh[PB], acc_r[PB], acc_i[PB], fd[PB];
   int gx[PB], gy[PB];
 #pragma unroll
@@ -251,11 +299,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     const int yl = (pi / kPatchesPerRow) * kPatchY + ly;
     gx[p] = i0 + xl;
     gy[p] = j0 + yl;
-    const double dux = (xl - 0.5 * (kTileX - 1)) * a.dx;
-    const double duy = (yl - 0.5 * (kTileY - 1)) * a.dy;
+    const double dux = (xl - 0.5 * (TX - 1)) * a.dx;
+    const double duy = (yl - 0.5 * (TY - 1)) * a.dy;
     ux[p] = (float)dux;
     uy[p] = (float)duy;
-    wh[p] = (float)(0.5 * (dux * dux + duy * duy));
+    wh[p] = (float)(dux * dux + duy * duy);   // |u|^2
     acc_r[p] = 0.f;
     acc_i[p] = 0.f;
     fd[p] = 0.f;
@@ -269,16 +317,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     wh[p] = __shfl_sync(0xffffffffu, wh[p], lane);
   }
   const float4* rec = reinterpret_cast<const float4*>(smem + L.rec);
-  const float A1 = a.A1f, C2 = a.C2f;
+  const float A1 = a.A1f, C3 = a.C3f;
 
+  int slot = 0;
+  uint32_t parity = 0;
   for (int it = 0; it < n_iter; ++it) {
-    const int slot = it % kBpStages;
-    const uint32_t parity = (it / kBpStages) & 1;
     mbar_wait(bar_full + 8 * slot, parity);
     const int cnt = min(a.CB, a.nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
     if (!BISTATIC) {
-#pragma unroll 1
+#pragma unroll kChirpUnroll
       for (int c = 0; c < cnt; ++c) {
         const float4 A = srec[2 * c], B = srec[2 * c + 1];
         const uint32_t off = __float_as_uint(B.w);
@@ -287,14 +335,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
           const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
           float kap = fmaf(A1, dR, B.y);
           if (DOP) kap += fd[p];
-          const float ph = fmaf(C2, dR, B.z);
           const float tk = kap + kMagic;
           const float kf = tk - kMagic;
           const float gf = kap - kf;
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
           const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
           float sn, cs;
-          __sincosf(ph, &sn, &cs);
+          __sincosf(C3 * gf, &sn, &cs);
           acc_r[p] = fmaf(vr, cs, acc_r[p]);
           acc_r[p] = fmaf(-vi, sn, acc_r[p]);
           acc_i[p] = fmaf(vr, sn, acc_i[p]);
@@ -318,14 +365,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
             const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
             float kap = fmaf(A1, dR, B.y);
             if (DOP) kap += fd[p];
-            const float ph = fmaf(C2, dR, B.z);
             const float tk = kap + kMagic;
             const float kf = tk - kMagic;
             const float gf = kap - kf;
             const float4 e = lds128(__float_as_uint(tk) * 16u + off);
             const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
             float sn, cs;
-            __sincosf(ph, &sn, &cs);
+            __sincosf(C3 * gf, &sn, &cs);
             acc_r[p] = fmaf(vr, cs, acc_r[p]);
             acc_r[p] = fmaf(-vi, sn, acc_r[p]);
             acc_i[p] = fmaf(vr, sn, acc_i[p]);
@@ -335,11 +381,23 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       }
     }
     mbar_arrive(bar_empty + 8 * slot);
+    if (++slot == S) {
+      slot = 0;
+      parity ^= 1;
+    }
   }
 
-  // epilogue: store (or accumulate) the tile
+  // epilogue: remove the Doppler index shift from the folded phase, then store (or
+  // accumulate) the tile
 #pragma unroll
   for (int p = 0; p < PB; ++p) {
+    if (DOP) {
+      float sn, cs;
+      sincosf(-C3 * fd[p], &sn, &cs);
+      const float r = acc_r[p] * cs - acc_i[p] * sn, i = acc_r[p] * sn + acc_i[p] * cs;
+      acc_r[p] = r;
+      acc_i[p] = i;
+    }
     if (gx[p] < a.nx && gy[p] < a.nrow) {
       float2* dst = a.img + (size_t)gy[p] * a.nx + gx[p];
       if (a.accumulate) {
@@ -352,39 +410,50 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   }
 }
 
-constexpr int kNCW = 8;   // consumer warps
-constexpr int kPB = 4;    // pixels per consumer thread
-static_assert(kNCW * kPB * kPatchX * kPatchY == kTileX * kTileY, "tile / warp map mismatch");
-
-template <bool BI, bool DOP, bool SAFE>
+template <bool BI, bool DOP, bool SAFE, int NCW, int PB>
 cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
-  auto kern = bp_kernel<BI, DOP, SAFE, kNCW, kPB>;
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, BI);
+  auto kern = bp_kernel<BI, DOP, SAFE, NCW, PB>;
+  constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
   static int configured_bytes = -1;
   if ((int)L.total > configured_bytes) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     configured_bytes = (int)L.total;
   }
-  const int tiles_y = (a.nrow + kTileY - 1) / kTileY;
+  const int tiles_y = (a.nrow + TY - 1) / TY;
   const long grid = (long)a.tiles_x * tiles_y;
-  kern<<<(unsigned)grid, (kNCW + 1) * 32, L.total, s>>>(a);
+  kern<<<(unsigned)grid, (NCW + 1) * 32, L.total, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int NCW, int PB>
+cudaError_t launch_shape(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s) {
+  if (bistatic) {
+    if (doppler) return safe ? launch_one<true, true, true, NCW, PB>(a, s) : launch_one<true, true, false, NCW, PB>(a, s);
+    return safe ? launch_one<true, false, true, NCW, PB>(a, s) : launch_one<true, false, false, NCW, PB>(a, s);
+  }
+  if (doppler) return safe ? launch_one<false, true, true, NCW, PB>(a, s) : launch_one<false, true, false, NCW, PB>(a, s);
+  return safe ? launch_one<false, false, true, NCW, PB>(a, s) : launch_one<false, false, false, NCW, PB>(a, s);
 }
 
 }  // namespace
 
-size_t bp_smem_bytes(int W, int CB, int n_rx, bool bistatic) {
-  return make_layout(W, CB, n_rx, bistatic).total;
+// Supported CTA shapes (consumer warps x pixels per thread); tile = 32 x (NCW * PB).
+bool bp_shape_supported(int ncw, int pb) {
+  return (ncw == 8 && pb == 4) || (ncw == 4 && pb == 8) || (ncw == 4 && pb == 4) || (ncw == 8 && pb == 8);
+}
+
+size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic) {
+  return make_layout(W, CB, n_rx, S, bistatic).total;
 }
 
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s) {
-  if (bistatic) {
-    if (doppler) return safe ? launch_one<true, true, true>(a, s) : launch_one<true, true, false>(a, s);
-    return safe ? launch_one<true, false, true>(a, s) : launch_one<true, false, false>(a, s);
-  }
-  if (doppler) return safe ? launch_one<false, true, true>(a, s) : launch_one<false, true, false>(a, s);
-  return safe ? launch_one<false, false, true>(a, s) : launch_one<false, false, false>(a, s);
+  if (a.ncw == 8 && a.pb == 4) return launch_shape<8, 4>(a, bistatic, doppler, safe, s);
+  if (a.ncw == 4 && a.pb == 8) return launch_shape<4, 8>(a, bistatic, doppler, safe, s);
+  if (a.ncw == 4 && a.pb == 4) return launch_shape<4, 4>(a, bistatic, doppler, safe, s);
+  if (a.ncw == 8 && a.pb == 8) return launch_shape<8, 8>(a, bistatic, doppler, safe, s);
+  return cudaErrorInvalidConfiguration;
 }
 
 }  // namespace sar

@@ -13,12 +13,10 @@ namespace sar {
 constexpr double kLightSpeed = 299792458.0;  // m/s
 constexpr double kPi = 3.14159265358979323846;
 
-// BP pixel tile of one CTA (see bp_kernel.cu for the warp/lane -> pixel map).
+// BP pixel tile of one CTA: 32 x (ncw * pb) pixels (see bp_kernel.cu for the
+// warp/lane -> pixel map).
 constexpr int kTileX = 32;
-constexpr int kTileY = 32;
-constexpr int kBpStages = 3;             // shared-memory ring depth
-constexpr int kBpMaxItemsPerStage = 32;  // (chirp, rx) windows per ring stage
-constexpr int kBpStageBudgetBytes = 24 * 1024;
+constexpr int kBpMaxStages = 8;          // shared-memory ring depth limit
 
 // Range-compression kernel arguments (rc_kernel.cu).
 struct RcArgs {
@@ -39,18 +37,22 @@ struct BpArgs {
   const double* tx;        // [n_chirps][3]
   const double* rx;        // [n_chirps][n_rx][3] or nullptr (monostatic)
   const float* dop;        // [ny][nx] or nullptr
+  const float2* binphase;  // [n_bins+1] exp(j 2 pi beta (k_lo + k + 1/2)), k = -1.., beta = c2/a1
   float2* img;             // [nrow][nx]
   int n_bins, n_rx, chirp0, nchirp, row0, nrow, nx, tiles_x, accumulate;
   int W;                   // window bins per item
   int CB;                  // chirps per ring stage
+  int S;                   // ring stages (<= kBpMaxStages)
+  int ncw, pb;             // CTA shape: consumer warps, pixels per consumer thread
   double x0, y0, z0, dx, dy;
   double a1, c2, k_lo;     // bins / metre two-way, cycles / metre two-way, crop start
   double kap_half;         // half window span in bins: 2 a1 rho + doppler bound
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
-  float C2f;               // phase slope (rad) per metre of Delta-R
+  float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };
 
-size_t bp_smem_bytes(int W, int CB, int n_rx, bool bistatic);
+bool bp_shape_supported(int ncw, int pb);
+size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s);
 
@@ -63,11 +65,13 @@ struct sar_plan_s {
   sar_plan_info_t info;
   int device;
   bool near_field;         // an antenna may come within 2 rho of a tile anchor
+  int bp_ncw, bp_pb, bp_stages;
   double tile_rho;         // tile half-diagonal (m)
   float rc_scale;
   float* d_window = nullptr;
   float2* d_twiddle = nullptr;
   float2* d_ramp = nullptr;
+  float2* d_binphase = nullptr;
   // sar_form_image workspace (lazily allocated)
   float* w_raw = nullptr;
   float* w_wsar = nullptr;

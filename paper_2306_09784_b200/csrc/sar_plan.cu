@@ -3,6 +3,7 @@
 // Citations: P:Lnnn = PAPER.md line (arXiv 2306.09784); A1..A17 = readings in DESIGN.md.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -45,6 +46,7 @@ struct Derived {
   sar_plan_info_t info;
   double rho;
   bool near_field;
+  int ncw, pb, stages;
 };
 
 // Host-side plan maths shared by sar_plan_geometry and sar_plan_create.
@@ -95,22 +97,40 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   I.k_lo = (int32_t)k_lo;
   I.n_bins = (int32_t)(k_hi - k_lo + 1);
 
+  // BP CTA shape and shared-memory ring (tuning override: SAR_BP_SHAPE="ncw,pb,stages,cb")
+  int ncw = 8, pb = 4, stages = 0, cb = 0;
+  if (const char* env = getenv("SAR_BP_SHAPE")) {
+    int v[4] = {0, 0, 0, 0};
+    if (sscanf(env, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]) >= 2 && sar::bp_shape_supported(v[0], v[1])) {
+      ncw = v[0];
+      pb = v[1];
+      stages = v[2];
+      cb = v[3];
+    }
+  }
+  out->ncw = ncw;
+  out->pb = pb;
   I.tile_x = sar::kTileX;
-  I.tile_y = sar::kTileY;
-  const double hx = 0.5 * (sar::kTileX - 1) * g->dx, hy = 0.5 * (sar::kTileY - 1) * g->dy;
+  I.tile_y = ncw * pb;  // 32-pixel-wide rows of 8x4 patches: tile area = 32 * ncw * pb
+  const double hx = 0.5 * (I.tile_x - 1) * g->dx, hy = 0.5 * (I.tile_y - 1) * g->dy;
   out->rho = sqrt(hx * hx + hy * hy) * (1.0 + 1e-9) + 1e-12;
   const double kap_half = 2.0 * I.a1_bins_per_m * out->rho + dop;
   const double w = ceil(2.0 * kap_half) + 4.0;
   if (w > 4096.0)
     return fail(SAR_ERR_INVALID_ARGUMENT,
-                "pixel spacing too coarse: a 32x32 tile spans more than 4096 range bins");
+                "pixel spacing too coarse: one BP tile spans more than 4096 range bins");
   I.window_bins = (int32_t)w;
   const bool bistatic = r->n_rx > 1;
-  const int item_bytes = I.window_bins * 16 + 32;
-  int items = std::max(1, std::min(sar::kBpMaxItemsPerStage, sar::kBpStageBudgetBytes / item_bytes));
-  int cb = std::max(1, items / r->n_rx);
+  if (cb <= 0) cb = std::max(1, 16 / r->n_rx);
+  const size_t stage_bytes = sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, 1, bistatic) - 16 * sar::kBpMaxStages;
+  if (stages <= 0) stages = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
+  stages = std::max(2, std::min(sar::kBpMaxStages, stages));
+  if (sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, stages, bistatic) > 200 * 1024)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "BP shared-memory ring does not fit (window too wide)");
   I.chirps_per_stage = cb;
-  (void)bistatic;
+  out->stages = stages;
+  if ((int64_t)r->n_chirps * r->n_rx * (I.n_bins + 1) >= (int64_t)1 << 31)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "n_chirps * n_rx * n_bins must stay below 2^31");
   I.updates_per_image = (int64_t)g->nx * g->ny * r->n_chirps * r->n_rx;
   out->near_field = dist_min < 2.0 * out->rho + 1e-3;
   return SAR_OK;
@@ -142,6 +162,7 @@ void free_plan(sar_plan_s* p) {
   cudaFree(p->d_window);
   cudaFree(p->d_twiddle);
   cudaFree(p->d_ramp);
+  cudaFree(p->d_binphase);
   cudaFree(p->w_raw);
   cudaFree(p->w_wsar);
   cudaFree(p->w_tx);
@@ -201,6 +222,9 @@ sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* 
   p->device = device;
   p->near_field = d.near_field;
   p->tile_rho = d.rho;
+  p->bp_ncw = d.ncw;
+  p->bp_pb = d.pb;
+  p->bp_stages = d.stages;
 
   // Constant tables, computed in double and rounded once to float32.
   const int ns = radar->n_samples, N = radar->fft_len, nb = d.info.n_bins;
@@ -225,14 +249,25 @@ sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* 
     const double ph = fmod(k * tc, (double)N) / (double)N;
     ramp[i] = make_float2((float)cos(2.0 * sar::kPi * ph), (float)sin(2.0 * sar::kPi * ph));
   }
+  // carrier phase of every crop bin's lower edge + half a bin: exp(j 2 pi beta (k + 1/2)),
+  // beta = c2 / a1 cycles per bin (the BP kernel's phase folding, bp_kernel.cu); entry i
+  // is crop bin i - 1 (from k = -1 up to n_bins - 1)
+  std::vector<float2> bph(nb + 1);
+  const double beta = d.info.c2_cycles_per_m / d.info.a1_bins_per_m;
+  for (int i = 0; i <= nb; ++i) {
+    double cyc = beta * ((double)(d.info.k_lo + i - 1) + 0.5);
+    cyc -= floor(cyc);
+    bph[i] = make_float2((float)cos(2.0 * sar::kPi * cyc), (float)sin(2.0 * sar::kPi * cyc));
+  }
   if ((st = dev_alloc(&p->d_window, ns)) != SAR_OK || (st = dev_alloc(&p->d_twiddle, tw.size())) != SAR_OK ||
-      (st = dev_alloc(&p->d_ramp, ramp.size())) != SAR_OK) {
+      (st = dev_alloc(&p->d_ramp, ramp.size())) != SAR_OK || (st = dev_alloc(&p->d_binphase, bph.size())) != SAR_OK) {
     free_plan(p);
     return st;
   }
   if ((e = cudaMemcpy(p->d_window, win.data(), ns * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(p->d_twiddle, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemcpy(p->d_ramp, ramp.data(), ramp.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      (e = cudaMemcpy(p->d_ramp, ramp.data(), ramp.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(p->d_binphase, bph.data(), bph.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(e, "cudaMemcpy (plan tables)");
   }
@@ -322,7 +357,10 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
   a.row0 = row0;
   a.nrow = nrow;
   a.nx = g.nx;
-  a.tiles_x = (g.nx + sar::kTileX - 1) / sar::kTileX;
+  a.tiles_x = (g.nx + plan->info.tile_x - 1) / plan->info.tile_x;
+  a.S = plan->bp_stages;
+  a.ncw = plan->bp_ncw;
+  a.pb = plan->bp_pb;
   a.accumulate = accumulate;
   a.W = plan->info.window_bins;
   a.CB = plan->info.chirps_per_stage;
@@ -337,7 +375,8 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
   a.kap_half = 2.0 * a.a1 * plan->tile_rho + (double)r.doppler_max_bins;
   const bool bistatic = rx_pos != nullptr;
   a.A1f = (float)(bistatic ? a.a1 : 2.0 * a.a1);
-  a.C2f = (float)(2.0 * sar::kPi * (bistatic ? a.c2 : 2.0 * a.c2));
+  a.binphase = plan->d_binphase;
+  a.C3f = (float)(2.0 * sar::kPi * a.c2 / a.a1);
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");

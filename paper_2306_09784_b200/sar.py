@@ -12,7 +12,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsar.so")
+LIB_PATH = os.environ.get("SAR_LIB", os.path.join(PKG, "libsar.so"))   # SAR_LIB: tuning builds
 
 SAR_OK = 0
 STATUS = {0: "SAR_OK", 1: "SAR_ERR_INVALID_ARGUMENT", 2: "SAR_ERR_OUT_OF_COVERAGE", 3: "SAR_ERR_CUDA",

@@ -261,7 +261,7 @@ def small_config(n_chirps=48, ns=128, nx=40, ny=24, n_rx=1, seed=11, curved=Fals
     grid = Grid(-0.4, 4.2, 0.0, grid_dx, grid_dx, nx, ny)
     pts, amps, iso = [], [], []
     for k in range(3):
-        mx, my = max(1, min(6, nx // 4)), max(1, min(3, ny // 4))
+        mx, my = min(6, nx // 4), min(3, ny // 4)
         i = int(rng.integers(mx, nx - mx)); j = int(rng.integers(my, ny - my))
         pts.append((grid.x0 + i * grid.dx, grid.y0 + j * grid.dy, 0.0))
         amps.append(rng.uniform(0.5, 1.0) * np.exp(1j * rng.uniform(0, 2 * np.pi)))

@@ -184,12 +184,18 @@ def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
     img, prof, plan = gpu_image(scn, raw, return_prof=True)
     tx = torch.as_tensor(scn.tx, device="cuda:0")
     rx = torch.as_tensor(scn.rx, device="cuda:0").contiguous()
+    ty = plan.info.tile_y
+    # shards on tile-row boundaries keep every tile anchor: bit-identical image
+    aligned = torch.cat([plan.backproject(prof, tx, rx, row0=r0, nrow=n) for r0, n in ((0, ty), (ty, 90 - ty))])
+    # arbitrary shards move the anchors: a different fp32 rounding pattern, each within the
+    # parity bar of the oracle; they agree to the accuracy of the anchored form
     rows = torch.cat([plan.backproject(prof, tx, rx, row0=r0, nrow=n) for r0, n in ((0, 23), (23, 40), (63, 27))])
     acc = plan.backproject(prof, tx, rx, chirp0=0, nchirp=37)
     plan.backproject(prof, tx, rx, chirp0=37, nchirp=63, out=acc, accumulate=True)
     torch.cuda.synchronize()
     a = img.cpu().numpy()
-    assert rel_err(rows.cpu().numpy(), a) < 1e-5
+    assert torch.equal(aligned, img)
+    assert rel_err(rows.cpu().numpy(), a) < 3e-4
     assert rel_err(acc.cpu().numpy(), a) < 1e-5
     # empty chirp shard: zeros (overwrite) / untouched (accumulate); empty row shard: no-op
     z = plan.backproject(prof, tx, rx, chirp0=10, nchirp=0)
