@@ -50,14 +50,8 @@ constexpr int kBatch = 8;                // producer: profile rows loaded per ba
 #define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
 #endif
 constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
-#ifndef SAR_BP_MINB_48
-#define SAR_BP_MINB_48 1                 // resident-CTA hint for the (4, 8) shape (register cap)
-#endif
-#ifndef SAR_BP_MINB_84
-#define SAR_BP_MINB_84 1
-#endif
-template <int NCW, int PB>
-constexpr int kMinBlocks = (NCW == 4 && PB == 8) ? SAR_BP_MINB_48 : (NCW == 8 && PB == 4) ? SAR_BP_MINB_84 : 1;
+// (A min-blocks launch bound, even "1", changes ptxas's schedule: measured 5 % slower on C3;
+//  capping registers for 6-7 resident CTAs spilled and was slower too.  tools/vsweep.sh)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -91,6 +85,47 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                : "r"(addr));
   return v;
 }
+
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2): one instruction, two round-to-nearest
+// fp32 operations.  A pair whose halves are equal is issued as a scalar broadcast operand,
+// so record values are read once for two pixels (the BP loop is register-file-read bound).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fsub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
 
 __device__ __forceinline__ float rsqrt_mufu(float x) {
   float y;
@@ -148,7 +183,7 @@ __host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bo
 }
 
 template <bool BISTATIC, bool DOP, bool SAFE, int NCW, int PB>
-__global__ void __launch_bounds__((NCW + 1) * 32, kMinBlocks<NCW, PB>) bp_kernel(const BpArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   constexpr int TX = kTileX;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -318,6 +353,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kMinBlocks<NCW, PB>) bp_kernel
   }
   const float4* rec = reinterpret_cast<const float4*>(smem + L.rec);
   const float A1 = a.A1f, C3 = a.C3f;
+  constexpr bool kPaired = !BISTATIC && !SAFE && (PB % 2 == 0);
+  f32x2 UX[PB / 2 + 1], UY[PB / 2 + 1], W2[PB / 2 + 1], FD2[PB / 2 + 1], ACC[PB + 1], ACI[PB + 1];
+  if (kPaired) {
+#pragma unroll
+    for (int h = 0; h < PB / 2; ++h) {
+      UX[h] = pk2(ux[2 * h], ux[2 * h + 1]);
+      UY[h] = pk2(uy[2 * h], uy[2 * h + 1]);
+      W2[h] = pk2(wh[2 * h], wh[2 * h + 1]);
+      FD2[h] = pk2(fd[2 * h], fd[2 * h + 1]);
+    }
+#pragma unroll
+    for (int p = 0; p < PB; ++p) ACC[p] = ACI[p] = pk2(0.f, 0.f);
+  }
 
   int slot = 0;
   uint32_t parity = 0;
@@ -325,7 +373,45 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kMinBlocks<NCW, PB>) bp_kernel
     mbar_wait(bar_full + 8 * slot, parity);
     const int cnt = min(a.CB, a.nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
-    if (!BISTATIC) {
+    if (kPaired) {
+      // Monostatic far field, pixels in pairs (2p, 2p+1): the range and index arithmetic
+      // runs as FFMA2/FADD2 over the pair with the record values as scalar broadcast
+      // operands; the complex interpolation and accumulation run as FFMA2 over (re, im).
+#pragma unroll kChirpUnroll
+      for (int c = 0; c < cnt; ++c) {
+        const float4 A = srec[2 * c], B = srec[2 * c + 1];
+        const uint32_t off = __float_as_uint(B.w);
+#pragma unroll
+        for (int h = 0; h < PB / 2; ++h) {
+          const f32x2 G2 = ffma2(bc2(A.x), UX[h], ffma2(bc2(A.y), UY[h], W2[h]));   // 2 D.u + |u|^2
+          const f32x2 S = fadd2(G2, bc2(A.z));                                       // ~|p - q|^2
+          const f32x2 Q = pk2(rsqrt_mufu(lo2(S)), rsqrt_mufu(hi2(S)));
+          const f32x2 T = ffma2(S, Q, bc2(-A.w));                                    // s q - r
+          const f32x2 H = ffma2(S, Q, bc2(A.w));                                     // s q + r
+          const f32x2 RHO = ffma2(pk2(-lo2(T), -hi2(T)), H, G2);                      // exact residual
+          const f32x2 DR = ffma2(RHO, fmul2(Q, bc2(0.5f)), T);                        // |p - q| - r
+          f32x2 KAP = ffma2(bc2(A1), DR, bc2(B.y));                                   // Alg. 2 L8
+          if (DOP) KAP = fadd2(KAP, FD2[h]);
+          const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
+          const f32x2 GF = fsub2(KAP, fsub2(TK, bc2(kMagic)));                        // gf in [-1/2, 1/2]
+          const f32x2 TH = fmul2(GF, bc2(C3));                                        // 2 pi beta gf
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float tk = k ? hi2(TK) : lo2(TK);
+            const float gf = k ? hi2(GF) : lo2(GF);
+            const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+            const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
+            float sn, cs;
+            __sincosf(k ? hi2(TH) : lo2(TH), &sn, &cs);
+            // v exp(j th) = vr (cs, sn) + vi (-sn, cs): the two halves go to separate
+            // accumulators, ACC += vr (cs, sn) and ACI += vi (sn, cs) (a swizzle, no
+            // negation); the epilogue forms (ACC.re - ACI.re, ACC.im + ACI.im)
+            ACC[2 * h + k] = ffma2(bc2(lo2(V)), pk2(cs, sn), ACC[2 * h + k]);
+            ACI[2 * h + k] = ffma2(bc2(hi2(V)), pk2(sn, cs), ACI[2 * h + k]);
+          }
+        }
+      }
+    } else if (!BISTATIC) {
 #pragma unroll kChirpUnroll
       for (int c = 0; c < cnt; ++c) {
         const float4 A = srec[2 * c], B = srec[2 * c + 1];
@@ -387,6 +473,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kMinBlocks<NCW, PB>) bp_kernel
     }
   }
 
+  if (kPaired) {
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      acc_r[p] = lo2(ACC[p]) - lo2(ACI[p]);
+      acc_i[p] = hi2(ACC[p]) + hi2(ACI[p]);
+    }
+  }
   // epilogue: remove the Doppler index shift from the folded phase, then store (or
   // accumulate) the tile
 #pragma unroll
