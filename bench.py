@@ -146,13 +146,19 @@ def _oracle_sample(scn, raw_np, target_s: float, nthreads: int = 0):
     t0 = time.perf_counter()
     prof = oracle.range_compress(raw_np, r.fft_len, r.range_window, scn.wsar, nthreads=nthreads)
     t_rc = time.perf_counter() - t0
-    # calibrate with a small probe, then size the sample
+    # calibrate with growing probes (each call also pays the wrapper's profile copy), then
+    # size the sample for about target_s seconds
     rng = np.random.default_rng(0)
-    probe = g.pixel_list(np.stack([rng.integers(0, g.ny, 32), rng.integers(0, g.nx, 32)], 1))
-    t0 = time.perf_counter()
-    oracle.backproject(prof, 0, r, scn.tx, scn.rx, probe, nthreads=nthreads)
-    t_probe = max(time.perf_counter() - t0, 1e-4)
-    n_pix = int(max(64, min(g.nx * g.ny, 32 * target_s / t_probe)))
+    n_probe, t_probe = 256, 0.0
+    while True:
+        probe = g.pixel_list(np.stack([rng.integers(0, g.ny, n_probe), rng.integers(0, g.nx, n_probe)], 1))
+        t0 = time.perf_counter()
+        oracle.backproject(prof, 0, r, scn.tx, scn.rx, probe, nthreads=nthreads)
+        t_probe = time.perf_counter() - t0
+        if t_probe > 0.1 * target_s or n_probe >= g.nx * g.ny:
+            break
+        n_probe *= 4
+    n_pix = int(max(64, min(g.nx * g.ny, n_probe * target_s / max(t_probe, 1e-4))))
     idx = np.stack([rng.integers(0, g.ny, n_pix), rng.integers(0, g.nx, n_pix)], 1)
     t0 = time.perf_counter()
     oracle.backproject(prof, 0, r, scn.tx, scn.rx, g.pixel_list(idx), nthreads=nthreads)
