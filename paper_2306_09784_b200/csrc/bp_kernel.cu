@@ -160,6 +160,18 @@ __device__ __forceinline__ float leg_delta(float D2x, float D2y, float r2, float
   }
 }
 
+// The far-field leg for a pixel pair (FFMA2 form of leg_delta<false>); record
+// A = {2Dx, 2Dy, r^2, r}.
+__device__ __forceinline__ f32x2 leg_delta2(const float4 A, const f32x2 UX, const f32x2 UY, const f32x2 W) {
+  const f32x2 G2 = ffma2(bc2(A.x), UX, ffma2(bc2(A.y), UY, W));   // 2 D.u + |u|^2
+  const f32x2 S = fadd2(G2, bc2(A.z));                            // ~|p - q|^2
+  const f32x2 Q = pk2(rsqrt_mufu(lo2(S)), rsqrt_mufu(hi2(S)));
+  const f32x2 T = ffma2(S, Q, bc2(-A.w));                         // s q - r
+  const f32x2 H = ffma2(S, Q, bc2(A.w));                          // s q + r
+  const f32x2 RHO = ffma2(pk2(-lo2(T), -hi2(T)), H, G2);          // exact residual
+  return ffma2(RHO, fmul2(Q, bc2(0.5f)), T);                      // |p - q| - r
+}
+
 // Shared-memory layout (bytes, 16-B aligned):
 //   [0, 128)                     mbarriers full[kBpMaxStages], empty[kBpMaxStages]
 //   rec   [S][LEGS] x 32 B       monostatic: LEGS = items; bistatic: LEGS = CB + items
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   }
   const float4* rec = reinterpret_cast<const float4*>(smem + L.rec);
   const float A1 = a.A1f, C3 = a.C3f;
-  constexpr bool kPaired = !BISTATIC && !SAFE && (PB % 2 == 0);
+  constexpr bool kPaired = !SAFE && (PB % 2 == 0);
   f32x2 UX[PB / 2 + 1], UY[PB / 2 + 1], W2[PB / 2 + 1], FD2[PB / 2 + 1], ACC[PB + 1], ACI[PB + 1];
   if (kPaired) {
 #pragma unroll
@@ -374,40 +386,51 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     const int cnt = min(a.CB, a.nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
     if (kPaired) {
-      // Monostatic far field, pixels in pairs (2p, 2p+1): the range and index arithmetic
-      // runs as FFMA2/FADD2 over the pair with the record values as scalar broadcast
-      // operands; the complex interpolation and accumulation run as FFMA2 over (re, im).
+      // Far field, pixels in pairs (2h, 2h+1): the range and index arithmetic runs as
+      // FFMA2/FADD2 over the pair with the record values as scalar broadcast operands; the
+      // complex interpolation and accumulation run as FFMA2 over (re, im).
+      // v exp(j th) = vr (cs, sn) + vi (-sn, cs): the two halves go to separate accumulators,
+      // ACC += vr (cs, sn) and ACI += vi (sn, cs) (a swizzle, no negation); the epilogue
+      // forms (ACC.re - ACI.re, ACC.im + ACI.im).
+      auto tail = [&](const int h, const f32x2 DR, const float kap_a, const uint32_t off) {
+        f32x2 KAP = ffma2(bc2(A1), DR, bc2(kap_a));                                   // Alg. 2 L8
+        if (DOP) KAP = fadd2(KAP, FD2[h]);
+        const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
+        const f32x2 GF = fsub2(KAP, fsub2(TK, bc2(kMagic)));                        // gf in [-1/2, 1/2]
+        const f32x2 TH = fmul2(GF, bc2(C3));                                        // 2 pi beta gf
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float tk = k ? hi2(TK) : lo2(TK);
+          const float gf = k ? hi2(GF) : lo2(GF);
+          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
+          float sn, cs;
+          __sincosf(k ? hi2(TH) : lo2(TH), &sn, &cs);
+          ACC[2 * h + k] = ffma2(bc2(lo2(V)), pk2(cs, sn), ACC[2 * h + k]);
+          ACI[2 * h + k] = ffma2(bc2(hi2(V)), pk2(sn, cs), ACI[2 * h + k]);
+        }
+      };
+      if (!BISTATIC) {
 #pragma unroll kChirpUnroll
-      for (int c = 0; c < cnt; ++c) {
-        const float4 A = srec[2 * c], B = srec[2 * c + 1];
-        const uint32_t off = __float_as_uint(B.w);
+        for (int c = 0; c < cnt; ++c) {
+          const float4 A = srec[2 * c], B = srec[2 * c + 1];
 #pragma unroll
-        for (int h = 0; h < PB / 2; ++h) {
-          const f32x2 G2 = ffma2(bc2(A.x), UX[h], ffma2(bc2(A.y), UY[h], W2[h]));   // 2 D.u + |u|^2
-          const f32x2 S = fadd2(G2, bc2(A.z));                                       // ~|p - q|^2
-          const f32x2 Q = pk2(rsqrt_mufu(lo2(S)), rsqrt_mufu(hi2(S)));
-          const f32x2 T = ffma2(S, Q, bc2(-A.w));                                    // s q - r
-          const f32x2 H = ffma2(S, Q, bc2(A.w));                                     // s q + r
-          const f32x2 RHO = ffma2(pk2(-lo2(T), -hi2(T)), H, G2);                      // exact residual
-          const f32x2 DR = ffma2(RHO, fmul2(Q, bc2(0.5f)), T);                        // |p - q| - r
-          f32x2 KAP = ffma2(bc2(A1), DR, bc2(B.y));                                   // Alg. 2 L8
-          if (DOP) KAP = fadd2(KAP, FD2[h]);
-          const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
-          const f32x2 GF = fsub2(KAP, fsub2(TK, bc2(kMagic)));                        // gf in [-1/2, 1/2]
-          const f32x2 TH = fmul2(GF, bc2(C3));                                        // 2 pi beta gf
+          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.y, __float_as_uint(B.w));
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+          const float4 T = srec[2 * c];
+          f32x2 DT[PB / 2];
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const float tk = k ? hi2(TK) : lo2(TK);
-            const float gf = k ? hi2(GF) : lo2(GF);
-            const float4 e = lds128(__float_as_uint(tk) * 16u + off);
-            const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
-            float sn, cs;
-            __sincosf(k ? hi2(TH) : lo2(TH), &sn, &cs);
-            // v exp(j th) = vr (cs, sn) + vi (-sn, cs): the two halves go to separate
-            // accumulators, ACC += vr (cs, sn) and ACI += vi (sn, cs) (a swizzle, no
-            // negation); the epilogue forms (ACC.re - ACI.re, ACC.im + ACI.im)
-            ACC[2 * h + k] = ffma2(bc2(lo2(V)), pk2(cs, sn), ACC[2 * h + k]);
-            ACI[2 * h + k] = ffma2(bc2(hi2(V)), pk2(sn, cs), ACI[2 * h + k]);
+          for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
+#pragma unroll 1
+          for (int n = 0; n < a.n_rx; ++n) {
+            const int ri = a.CB + c * a.n_rx + n;
+            const float4 A = srec[2 * ri], B = srec[2 * ri + 1];
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h)
+              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.y, __float_as_uint(B.w));
           }
         }
       }
