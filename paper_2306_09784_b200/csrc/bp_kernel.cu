@@ -37,6 +37,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "sar_internal.h"
 
 namespace sar {
@@ -205,7 +207,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpMaxStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int tile = blockIdx.x;
+  // CTA -> (chirp chunk, tile), chunk-major so that concurrently resident CTAs stream the
+  // same profile rows through L2.  ksplit > 1 only for grids too small to fill the GPU.
+  const int ntiles = a.tiles_x * a.tiles_y;
+  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int chirp0 = a.chirp0 + chunk * a.chunk;
+  const int nchirp = min(a.chunk, a.nchirp - chunk * a.chunk);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int i0 = tx * TX;               // first grid column of the tile
   const int j0 = ty * TY;               // first row of the tile, relative to row0
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   }
   __syncthreads();
 
-  const int n_iter = (a.nchirp + a.CB - 1) / a.CB;
+  const int n_iter = (nchirp + a.CB - 1) / a.CB;
 
   if (warp == NCW) {
     // ============================== PRODUCER ==============================
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     for (int it = 0; it < n_iter; ++it) {
       mbar_wait(bar_empty + 8 * slot, parity ^ 1);
       const int c0 = it * a.CB;
-      const int cnt = min(a.CB, a.nchirp - c0);
+      const int cnt = min(a.CB, nchirp - c0);
       const int items = cnt * a.n_rx;
       float4* srec = rec + (size_t)slot * L.legs * 2;
       int2* skw = kwin + slot * L.items;
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       // ---- anchor records (fp64), one item per lane
       if (BISTATIC) {
         for (int c = lane; c < cnt; c += 32) {
-          const double* q = a.tx + 3 * (size_t)(a.chirp0 + c0 + c);
+          const double* q = a.tx + 3 * (size_t)(chirp0 + c0 + c);
           const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       for (int e = lane; e < items; e += 32) {
         const int c = BISTATIC ? e / a.n_rx : e;
         const int n = BISTATIC ? e - c * a.n_rx : 0;
-        const int m = a.chirp0 + c0 + c;
+        const int m = chirp0 + c0 + c;
         const double* qt = a.tx + 3 * (size_t)m;
         // The consumers form r32 + dR = sqrt(r32^2 + 2 D32.u + |u|^2) from the fp32-rounded
         // record; the anchor path length uses the exact fp64 |D| so that the rounding of
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   uint32_t parity = 0;
   for (int it = 0; it < n_iter; ++it) {
     mbar_wait(bar_full + 8 * slot, parity);
-    const int cnt = min(a.CB, a.nchirp - it * a.CB);
+    const int cnt = min(a.CB, nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
     if (kPaired) {
       // Far field, pixels in pairs (2h, 2h+1): the range and index arithmetic runs as
@@ -516,7 +523,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     }
     if (gx[p] < a.nx && gy[p] < a.nrow) {
       float2* dst = a.img + (size_t)gy[p] * a.nx + gx[p];
-      if (a.accumulate) {
+      if (a.ksplit > 1) {
+        // several chirp chunks add into the same pixel (the image was zeroed first when
+        // not accumulating); fire-and-forget reductions in L2
+        float* d = reinterpret_cast<float*>(dst);
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+      } else if (a.accumulate) {
         const float2 o = *dst;
         *dst = make_float2(o.x + acc_r[p], o.y + acc_i[p]);
       } else {
@@ -537,9 +550,29 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured_bytes = (int)L.total;
   }
-  const int tiles_y = (a.nrow + TY - 1) / TY;
-  const long grid = (long)a.tiles_x * tiles_y;
-  kern<<<(unsigned)grid, (NCW + 1) * 32, L.total, s>>>(a);
+  BpArgs b = a;
+  b.tiles_y = (a.nrow + TY - 1) / TY;
+  const long ntiles = (long)b.tiles_x * b.tiles_y;
+  // Chirp split for grids that cannot fill the GPU: enough CTAs for ~8 waves of resident
+  // CTAs, each chunk at least 512 chirps (and a multiple of the ring stage).
+  int resident = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, (NCW + 1) * 32, L.total);
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long slots = (long)std::max(1, resident) * sms;
+  int k = 1;
+  while (ntiles * k < 8 * slots && a.nchirp / (2 * k) >= 512) k *= 2;
+  b.chunk = (a.nchirp + k - 1) / k;
+  b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
+  b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);
+  if (b.ksplit < 1) b.ksplit = 1;
+  if (b.ksplit > 1 && !a.accumulate) {
+    cudaError_t e = cudaMemsetAsync(a.img, 0, sizeof(float2) * (size_t)a.nrow * a.nx, s);
+    if (e != cudaSuccess) return e;
+  }
+  const long grid = ntiles * b.ksplit;
+  kern<<<(unsigned)grid, (NCW + 1) * 32, L.total, s>>>(b);
   return cudaGetLastError();
 }
 

@@ -40,6 +40,8 @@ struct BpArgs {
   const float2* binphase;  // [n_bins+1] exp(j 2 pi beta (k_lo + k + 1/2)), k = -1.., beta = c2/a1
   float2* img;             // [nrow][nx]
   int n_bins, n_rx, chirp0, nchirp, row0, nrow, nx, tiles_x, accumulate;
+  int tiles_y;              // set by the launcher
+  int ksplit, chunk;        // chirp split (launcher): ksplit chunks of `chunk` chirps
   int W;                   // window bins per item
   int CB;                  // chirps per ring stage
   int S;                   // ring stages (<= kBpMaxStages)

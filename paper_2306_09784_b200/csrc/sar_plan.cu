@@ -121,7 +121,7 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
                 "pixel spacing too coarse: one BP tile spans more than 4096 range bins");
   I.window_bins = (int32_t)w;
   const bool bistatic = r->n_rx > 1;
-  if (cb <= 0) cb = std::max(1, 16 / r->n_rx);
+  if (cb <= 0) cb = std::max(1, 32 / r->n_rx);
   const size_t stage_bytes = sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, 1, bistatic) - 16 * sar::kBpMaxStages;
   if (stages <= 0) stages = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
   stages = std::max(2, std::min(sar::kBpMaxStages, stages));

@@ -207,6 +207,24 @@ def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
     plan.close()
 
 
+def test_chirp_split_for_small_grids(cuda_lib):
+    """A grid of few tiles and many chirps runs as several chirp chunks per tile that add into
+    the image (red.global.add); overwrite and accumulate both match the oracle."""
+    import torch
+
+    scn = sarsim.small_config(n_chirps=2048, ns=256, nx=48, ny=40, seed=45, curved=True)
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert rel_err(img.cpu().numpy().reshape(-1), ref) <= REL_TOL
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    twice = img.clone()
+    plan.backproject(prof, tx, out=twice, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_err(twice.cpu().numpy(), 2 * img.cpu().numpy()) < 1e-6
+    plan.close()
+
+
 def test_one_pixel_grid_and_single_chirp(cuda_lib):
     scn = sarsim.small_config(n_chirps=1, ns=128, nx=1, ny=1, seed=42)
     raw = _raw(scn)
