@@ -199,7 +199,8 @@ def make_config(name: str, n_chirps: int | None = None, seed: int | None = None,
         scn = Scenario("C1", radar, grid, tx, None, tgt, amp, iso, None, 0.0, seed or 1)
     elif name in ("C2", "C0", "C5"):
         radar = Radar()
-        M = n_chirps or 8192
+        # C5: one long straight track of 8192 + 15 hops of 1024 chirps (16 frames)
+        M = n_chirps or (8192 + 15 * 1024 if name == "C5" else 8192)
         step = 8.0 * radar.pri_s
         tx = straight_track(M, step)
         if name == "C2":
@@ -246,6 +247,23 @@ def make_config(name: str, n_chirps: int | None = None, seed: int | None = None,
     else:
         raise ValueError(wsar)
     return scn
+
+
+def c5_frames(scn: Scenario, hop: int = 1024, aperture: int = 8192, n_frames: int | None = None):
+    """C5 streaming frames: frame f uses chirps [f hop, f hop + aperture) and the
+    C2 grid (3000 x 1200 at 1 cm) re-centred in x on the frame's aperture centre, snapped to the
+    pixel pitch.  One frame per hop = one paper measurement of N_m T_P0 = 109.3 ms.
+    Returns [(chirp0, Grid)]."""
+    g = scn.grid
+    total = (scn.n_chirps - aperture) // hop + 1
+    n = total if n_frames is None else min(n_frames, total)
+    frames = []
+    for f in range(n):
+        c0 = f * hop
+        xc = float(np.mean(scn.tx[c0:c0 + aperture, 0]))
+        x0 = round((xc - 0.5 * (g.nx - 1) * g.dx) / g.dx) * g.dx
+        frames.append((c0, Grid(x0, g.y0, g.z0, g.dx, g.dy, g.nx, g.ny)))
+    return frames
 
 
 def small_config(n_chirps=48, ns=128, nx=40, ny=24, n_rx=1, seed=11, curved=False,

@@ -276,6 +276,40 @@ def test_form_image_host_buffers_equal_device_path(cuda_lib):
     plan.close()
 
 
+# ----------------------------------------------------------------------------- C5 streaming
+def test_C5_streaming_frame_sampled_parity_and_chirp_shards(cuda_lib):
+    """One C5 frame (chirps [f H, f H + 8192) of the long track, grid re-centred on the frame):
+    sampled parity against the oracle, and the frame as the sum of 4 chirp shards (the chirp-
+    sharded multi-GPU decomposition, accumulated on one GPU) equals the one-shot frame."""
+    import torch
+
+    scn = sarsim.make_config("C5")
+    frames = sarsim.c5_frames(scn)
+    c0, grid = frames[9]
+    raw = _raw(scn)
+    lo, hi = scn.antenna_box(1e-3)
+    plan = cuda_lib.Plan(scn.radar, grid, scn.n_chirps, 1, (lo, hi))
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    prof = plan.empty_profiles()
+    plan.range_compress(raw, chirp0=c0, nchirp=8192, out=prof)
+    img = plan.backproject(prof, tx, chirp0=c0, nchirp=8192)
+    acc = torch.zeros_like(img)
+    for k in range(4):
+        plan.backproject(prof, tx, chirp0=c0 + 2048 * k, nchirp=2048, out=acc, accumulate=True)
+    torch.cuda.synchronize()
+    a = img.cpu().numpy()
+    assert rel_err(acc.cpu().numpy(), a) < 1e-5
+    sub = sarsim.Scenario("C5f", scn.radar, grid, scn.tx[c0:c0 + 8192], None, scn.targets, scn.amps,
+                          np.zeros((0, 2), int), scn.wsar[c0:c0 + 8192])
+    idx = sample_indices(sub, np.abs(a), stride=(97, 101), win=2)
+    ref_prof = oracle_profiles(sub, raw[c0:c0 + 8192].cpu().numpy(), plan.k_lo, plan.n_bins)
+    ref = oracle.backproject(ref_prof, plan.k_lo, scn.radar, sub.tx, None, grid.pixel_list(idx))
+    got = a[idx[:, 0], idx[:, 1]]
+    plan.close()
+    assert rel_err(got, ref) <= REL_TOL
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+
+
 # ----------------------------------------------------------------------------- full-size configs
 @pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4"])
 def test_full_size_config_sampled_parity(cuda_lib, cfg):
