@@ -169,6 +169,20 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
                             const float* doppler_host, int32_t row0, int32_t nrow,
                             sar_complex64_t* image_host, sar_stream_t stream);
 
+/* Per-pixel Doppler index shift of Measure D (Alg. 2 L8 f_doppler(p)): "the
+ * radial component for every pixel p can be calculated in advance based on the average
+ * vehicle velocity".  For pixel p of `grid`:
+ *   v_r(p) = n_legs <p - q_ref, v_avg> / |p - q_ref|     (TX and RX legs, n_legs = 2)
+ *   f_doppler(p) = (f0 v_r(p) / c) / (fs / N_fft)        in profile bins,
+ * with q_ref the aperture-centre antenna position and v_avg the average velocity (host,
+ * metres and m/s).  |f_doppler| <= 2 f0 |v_avg| N_fft / (c fs): declare that bound (or the
+ * table's max) as doppler_max_bins in the plan that consumes the table.
+ *   doppler_bins  dev float [ny][nx] (written); a pixel at q_ref gets 0.
+ * Computed on `stream` in fp64, stored as float32.  No plan needed. */
+sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                               const double q_ref[3], const double v_avg[3], float* doppler_bins,
+                               sar_stream_t stream);
+
 /* Number of CUDA kernels this plan has launched since creation. */
 int64_t sar_plan_launch_count(sar_plan_t plan);
 

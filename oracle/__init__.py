@@ -14,6 +14,7 @@ Functions and the passages they follow (P:Lnnn = PAPER.md line):
   fft               textbook radix-2 FFT (a library-primitive step)
   range_compress    H1, windowed zero-padded range FFT with centring ramp (A4-A8)
   backproject       H3-H5, Alg. 2 with Alg. 1 constants
+  doppler_table     Measure D f_doppler(p) from the average velocity
 All are pinned by tests/test_oracle_pins.py (no function is "parity unpinned").
 """
 from __future__ import annotations
@@ -58,7 +59,8 @@ def _load():
             lib.oracle_range_compress.argtypes = [P(f), i, i, i, i, i, P(d), i, i, i, i, P(d)]
             lib.oracle_backproject.argtypes = [P(d), i, i, i, i, d, d, d, d, i,
                                                P(d), P(d), P(d), P(d), i, i, P(d)]
-            for name in ("oracle_window", "oracle_dft_row", "oracle_fft",
+            lib.oracle_doppler_table.argtypes = [d, d, i, P(d), i, P(d), P(d), d, P(d)]
+            for name in ("oracle_window", "oracle_dft_row", "oracle_fft", "oracle_doppler_table",
                          "oracle_range_compress", "oracle_backproject", "oracle_version"):
                 getattr(lib, name).restype = ctypes.c_int
             _lib = lib
@@ -140,3 +142,16 @@ def backproject(prof, k0: int, radar, tx, rx, pixels, doppler=None, nthreads: in
         _ptr(tx, ctypes.c_double), _ptr(rxa, ctypes.c_double), _ptr(dop, ctypes.c_double),
         _ptr(pix, ctypes.c_double), pix.shape[0], nthreads, _ptr(out, ctypes.c_double)), "backproject")
     return out[:, 0] + 1j * out[:, 1]
+
+
+def doppler_table(radar, pixels, q_ref, v_avg, legs: float = 2.0) -> np.ndarray:
+    """f_doppler(p) in bins for pixels [P][3] (Measure D)."""
+    pix = np.ascontiguousarray(pixels, np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(q_ref, np.float64).reshape(3)
+    v = np.ascontiguousarray(v_avg, np.float64).reshape(3)
+    out = np.empty(pix.shape[0], np.float64)
+    _check(_load().oracle_doppler_table(float(radar.f0_hz), float(radar.sample_rate_hz), int(radar.fft_len),
+                                        _ptr(pix, ctypes.c_double), pix.shape[0], _ptr(q, ctypes.c_double),
+                                        _ptr(v, ctypes.c_double), float(legs), _ptr(out, ctypes.c_double)),
+           "doppler_table")
+    return out

@@ -315,3 +315,23 @@ int oracle_backproject(const double* prof, int n_chirps, int n_rx, int k0, int n
   free(th); free(jobs);
   return status;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Measure D: per-pixel Doppler index shift f_doppler(p) of Alg. 2 */
+/* L8, "calculated in advance based on the average vehicle velocity":  */
+/*   v_r(p) = legs * <p - q_ref, v_avg> / |p - q_ref|   (Alg. 1 L5, L8, L9 with   */
+/*            one velocity for the whole aperture; legs = 2 for TX + RX)        */
+/*   f_doppler(p) = (f0 * v_r(p) / c) / (fs / N)         (Alg. 1 L11, in bins)  */
+/* A pixel at q_ref gets 0.                                                    */
+/* ------------------------------------------------------------------------- */
+int oracle_doppler_table(double f0_hz, double fs_hz, int nfft, const double* pix, int n_pix,
+                         const double* q_ref, const double* v_avg, double legs, double* out) {
+  if (!pix || !q_ref || !v_avg || !out || n_pix < 0 || fs_hz <= 0 || nfft < 1) return -1;
+  for (int p = 0; p < n_pix; ++p) {
+    const double dx = pix[3 * p] - q_ref[0], dy = pix[3 * p + 1] - q_ref[1], dz = pix[3 * p + 2] - q_ref[2];
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double vr = r > 0.0 ? legs * (dx * v_avg[0] + dy * v_avg[1] + dz * v_avg[2]) / r : 0.0;
+    out[p] = (f0_hz * vr / ORACLE_C_LIGHT) / (fs_hz / (double)nfft);
+  }
+  return 0;
+}

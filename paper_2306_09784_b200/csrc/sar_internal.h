@@ -58,6 +58,17 @@ size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s);
 
+// Doppler-table kernel arguments (doppler_kernel.cu).
+struct DopArgs {
+  float* out;              // [ny][nx]
+  double x0, y0, z0, dx, dy;
+  int nx, ny;
+  double q[3], v[3];       // reference antenna position, average velocity
+  double legs;             // 2: TX and RX legs
+  double bins_per_mps;     // f0 / c / (fs / N): bins per m/s of radial speed
+};
+cudaError_t launch_doppler(const DopArgs& a, cudaStream_t s);
+
 }  // namespace sar
 
 struct sar_plan_s {

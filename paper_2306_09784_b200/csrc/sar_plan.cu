@@ -447,6 +447,37 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   return SAR_OK;
 }
 
+sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                               const double q_ref[3], const double v_avg[3], float* doppler_bins,
+                               sar_stream_t stream) {
+  if (!radar || !grid || !q_ref || !v_avg || !doppler_bins)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (!finite_pos(radar->f0_hz) || !finite_pos(radar->sample_rate_hz) || radar->fft_len < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "f0_hz, sample_rate_hz and fft_len must be positive");
+  if (!finite_pos(grid->dx) || !finite_pos(grid->dy) || grid->nx < 1 || grid->ny < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "grid needs dx, dy > 0 and nx, ny >= 1");
+  for (int k = 0; k < 3; ++k)
+    if (!isfinite(q_ref[k]) || !isfinite(v_avg[k])) return fail(SAR_ERR_INVALID_ARGUMENT, "non-finite q_ref/v_avg");
+  sar::DopArgs a;
+  a.out = doppler_bins;
+  a.x0 = grid->x0;
+  a.y0 = grid->y0;
+  a.z0 = grid->z0;
+  a.dx = grid->dx;
+  a.dy = grid->dy;
+  a.nx = grid->nx;
+  a.ny = grid->ny;
+  for (int k = 0; k < 3; ++k) {
+    a.q[k] = q_ref[k];
+    a.v[k] = v_avg[k];
+  }
+  a.legs = 2.0;
+  a.bins_per_mps = radar->f0_hz / sar::kLightSpeed / (radar->sample_rate_hz / radar->fft_len);
+  cudaError_t e = sar::launch_doppler(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "doppler table launch");
+  return SAR_OK;
+}
+
 sar_status_t sar_destroy(sar_plan_t plan) {
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   DeviceGuard guard(plan->device);

@@ -74,6 +74,9 @@ def load() -> ctypes.CDLL:
             lib.sar_range_compress.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_backproject.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp]
             lib.sar_form_image.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]
+            lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
+                                              P(ctypes.c_double * 3), _vp, _vp]
+            lib.sar_doppler_table.restype = ctypes.c_int
             lib.sar_plan_launch_count.argtypes = [_vp]
             lib.sar_plan_launch_count.restype = ctypes.c_int64
             lib.sar_destroy.argtypes = [_vp]
@@ -128,6 +131,31 @@ def sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row
 
 def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream=0):
     _check(load().sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream))
+
+
+def sar_doppler_table(radar: RadarParams, grid: Grid, q_ref, v_avg, dop_ptr, stream=0):
+    q = (ctypes.c_double * 3)(*[float(v) for v in q_ref])
+    v = (ctypes.c_double * 3)(*[float(x) for x in v_avg])
+    _check(load().sar_doppler_table(ctypes.byref(radar), ctypes.byref(grid), ctypes.byref(q), ctypes.byref(v),
+                                    dop_ptr, stream))
+
+
+def doppler_bound_bins(radar, v_avg) -> float:
+    """|f_doppler| <= 2 f0 |v_avg| N / (c fs): a valid doppler_max_bins for a plan."""
+    import math
+
+    speed = math.sqrt(sum(float(x) ** 2 for x in v_avg))
+    return 2.0 * radar.f0_hz * speed / 299792458.0 * radar.fft_len / radar.sample_rate_hz
+
+
+def doppler_table(radar, grid, q_ref, v_avg, device=0, out=None, stream=None):
+    """Measure D table (float32 [ny][nx], CUDA) via sar_doppler_table."""
+    import torch
+
+    out = torch.empty((grid.ny, grid.nx), dtype=torch.float32, device=f"cuda:{device}") if out is None else out
+    sar_doppler_table(radar_params(radar, 1, 1), grid_params(grid), q_ref, v_avg,
+                      _dptr(out, torch.float32, (grid.ny, grid.nx), "doppler"), _stream_handle(stream))
+    return out
 
 
 def sar_plan_launch_count(plan) -> int:

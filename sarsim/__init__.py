@@ -289,8 +289,17 @@ def small_config(n_chirps=48, ns=128, nx=40, ny=24, n_rx=1, seed=11, curved=Fals
 
 
 # ----------------------------------------------------------------------------- raw beat
+def track_velocity(scn: Scenario) -> np.ndarray:
+    """Per-chirp platform velocity [M][3] (central differences of the TX track over T_P0)."""
+    q = scn.tx
+    if q.shape[0] < 2:
+        return np.zeros_like(q)
+    v = np.gradient(q, axis=0) / scn.radar.pri_s
+    return v
+
+
 def simulate_raw(scn: Scenario, device: str = "cpu", chirp_block: int = 64,
-                 targets=None, amps=None):
+                 targets=None, amps=None, doppler: bool = False):
     """Real FMCW beat samples float32 [M][N_rx][Ns] of a stop-and-go point scene.
 
     For scatterer k with complex reflectivity a_k and two-way path
@@ -298,7 +307,10 @@ def simulate_raw(scn: Scenario, device: str = "cpu", chirp_block: int = 64,
         x[t] = sum_k |a_k| cos(2 pi mu tau (t - t_c)/fs - 2 pi f0 tau + arg a_k)
     with mu = B/T_P (P:L200), t_c = (Ns-1)/2 and f0 the centre frequency (A4);
     the positive-frequency component carries phase -2 pi f0 tau (A2).  No range
-    decay, no residual video phase (A11), no Doppler within the chirp (A10).
+    decay, no residual video phase (A11).  Stop-and-go by default; with ``doppler=True``
+    the beat frequency carries the Doppler term of Alg. 1 L5, L8, L9, L11:
+    mu tau + f0 (v_tx + v_rx)/c with v_tx = <p - q_tx, v(m)>/|p - q_tx| (same for RX) and
+    v(m) the platform velocity (A10).
     AWGN of std ``noise_sigma`` per sample from a seeded torch generator.
     Computed in float64 (torch, on ``device``), returned as a float32 torch tensor.
     """
@@ -332,6 +344,16 @@ def simulate_raw(scn: Scenario, device: str = "cpu", chirp_block: int = 64,
         cyc_f0 = r.f0_hz * tau
         ph0 = -2.0 * math.pi * (cyc_f0 - torch.floor(cyc_f0)) + arg                 # [b,n,K]
         fb = mu * tau / fs                                                           # cycles/sample
+        if doppler:
+            vel = torch.as_tensor(track_velocity(scn)[m0:m1], dtype=f64, device=dev)  # [b,3]
+            ut = (P[None, :, :] - tx[m0:m1, None, :]) / dtx[..., None]               # [b,K,3]
+            v_tx = (ut * vel[:, None, :]).sum(-1)                                     # Alg. 1 L5
+            if rx is None:
+                v = (2.0 * v_tx)[:, None, :]
+            else:
+                ur = (P[None, None, :, :] - rx[m0:m1, :, None, :]) / drx[..., None]
+                v = v_tx[:, None, :] + (ur * vel[:, None, None, :]).sum(-1)           # Alg. 1 L8, L9
+            fb = fb + r.f0_hz * v / C_LIGHT / fs                                      # Alg. 1 L11
         acc = torch.zeros((m1 - m0, nrx, ns), dtype=f64, device=dev)
         for k0 in range(0, len(tg), kb):
             k1 = min(len(tg), k0 + kb)
