@@ -399,7 +399,27 @@ def run_stream(args):
     stream = torch.cuda.current_stream(dev)
     c_lo, c_n = chirp_partition(8192, world, rank)
 
+    incremental = args.config == "C5i"
+    if incremental:
+        # NEXT-2: world-fixed grid (the C2 grid), one partial image per 1024-chirp hop in a ring
+        # of 8; a frame = back-projection of the newest hop + sum of the ring
+        g0 = scn.grid
+        plans.append(sar.Plan(scn.radar, g0, scn.n_chirps, 1, (lo, hi), device=local))
+        ring = torch.zeros((8, g0.ny, g0.nx), dtype=torch.complex64, device=dev)
+        iplan = plans[-1]
+        iprof = iplan.empty_profiles()
+        h_lo, h_n = chirp_partition(1024, world, rank)
+        img = torch.empty((g0.ny, g0.nx), dtype=torch.complex64, device=dev)
+
     def frame(f):
+        if incremental:
+            h = f % (scn.n_chirps // 1024)
+            iplan.range_compress(raw, wsar, chirp0=h * 1024 + h_lo, nchirp=h_n, out=iprof, stream=stream)
+            iplan.backproject(iprof, tx, chirp0=h * 1024 + h_lo, nchirp=h_n, out=ring[h % 8], stream=stream)
+            if world > 1:
+                reduce_partials(ring[h % 8], dst=0)
+            sar.image_sum(ring, out=img, stream=stream)
+            return
         c0, _ = frames[f % len(frames)]
         plan = plans[f % len(frames)]
         prof = prof_buf[: scn.n_chirps * plan.n_bins].view(scn.n_chirps, 1, plan.n_bins)
@@ -428,18 +448,25 @@ def run_stream(args):
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_frame = float(tot[0]) / args.steps
-    upd = g0.nx * g0.ny * 8192
+    upd = g0.nx * g0.ny * 8192          # updates of the frame's 8192-chirp image
+    if incremental:
+        workload = ("C5i (NEXT-2 incremental): world-fixed 30 m x 12 m grid at 1 cm, 8 partial images of "
+                    "1024-chirp hops in a ring; a frame = BP of the newest hop + ring sum")
+        step = "one frame: sar_range_compress + sar_backproject of one hop (+ reduce) + sar_image_sum"
+    else:
+        workload = ("C5: 16 frames of 8192 chirps, 1024-chirp hop, straight 8 m/s track, "
+                    "30 m x 12 m grid at 1 cm re-centred per frame")
+        step = "one frame: sar_range_compress + sar_backproject of this rank's chirps (+ reduce)"
     if rank == 0:
         print(json.dumps({
-            "metric": "ms per 8192-chirp C5 streaming frame; pixel·chirp updates/s",
+            "metric": "ms per 8192-chirp streaming frame; image pixel·chirp updates/s",
             "value": upd / (ms_frame * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_frame, "max_frame_ms": float(tot[1]),
             "realtime_budget_ms": 1024 * scn.radar.pri_s * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C5: 16 frames of 8192 chirps, 1024-chirp hop, straight 8 m/s track, "
-                                   "30 m x 12 m grid at 1 cm re-centred per frame",
-                       "config": "C5", "parallelism": f"chirps x{world}" + (" + NCCL reduce" if world > 1 else ""),
-                       "step": "one frame: sar_range_compress + sar_backproject of this rank's chirps (+ reduce)"},
+            "config": {"workload": workload, "config": args.config,
+                       "parallelism": f"chirps x{world}" + (" + NCCL reduce" if world > 1 else ""),
+                       "step": step},
             "gpu_launches": launches, "clocks": clk.summary(),
         }), flush=True)
     for p in plans:
@@ -454,7 +481,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS) + ["C5"])
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS) + ["C5", "C5i"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
@@ -463,10 +490,10 @@ def main(argv=None):
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
-        if args.config == "C5":
+        if args.config in ("C5", "C5i"):
             raise SystemExit("--impl reference supports the image configs (C0-C4)")
         return run_reference(args)
-    return run_stream(args) if args.config == "C5" else run_ours(args)
+    return run_stream(args) if args.config in ("C5", "C5i") else run_ours(args)
 
 
 if __name__ == "__main__":

@@ -183,6 +183,15 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
                                const double q_ref[3], const double v_avg[3], float* doppler_bins,
                                sar_stream_t stream);
 
+/* Incremental streaming (NEXT-2; continuous processing): with a
+ * world-fixed grid, a frame over an aperture of n_partials hops is the sum of the hops'
+ * partial images (each sar_backproject over one hop of chirps).  Writes
+ *   out[i] = sum_{k < n_partials} partials[k * stride + i],  i < n_elems
+ * summed in k order (deterministic).  partials: dev complex ring [n_partials][stride];
+ * out: dev complex [n_elems].  n_partials >= 1, stride >= n_elems. */
+sar_status_t sar_image_sum(sar_complex64_t* out, const sar_complex64_t* partials, int32_t n_partials,
+                           int64_t stride, int64_t n_elems, sar_stream_t stream);
+
 /* Number of CUDA kernels this plan has launched since creation. */
 int64_t sar_plan_launch_count(sar_plan_t plan);
 

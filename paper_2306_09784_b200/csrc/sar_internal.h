@@ -68,6 +68,7 @@ struct DopArgs {
   double bins_per_mps;     // f0 / c / (fs / N): bins per m/s of radial speed
 };
 cudaError_t launch_doppler(const DopArgs& a, cudaStream_t s);
+cudaError_t launch_sum(float2* out, const float2* in, int n, long stride, long count, cudaStream_t s);
 
 }  // namespace sar
 

@@ -478,6 +478,18 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
   return SAR_OK;
 }
 
+sar_status_t sar_image_sum(sar_complex64_t* out, const sar_complex64_t* partials, int32_t n_partials,
+                           int64_t stride, int64_t n_elems, sar_stream_t stream) {
+  if (!out || !partials) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_partials < 1 || n_elems < 0 || stride < n_elems)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "need n_partials >= 1 and stride >= n_elems >= 0");
+  if (n_elems == 0) return SAR_OK;
+  cudaError_t e = sar::launch_sum(reinterpret_cast<float2*>(out), reinterpret_cast<const float2*>(partials),
+                                  n_partials, (long)stride, (long)n_elems, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "image sum launch");
+  return SAR_OK;
+}
+
 sar_status_t sar_destroy(sar_plan_t plan) {
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   DeviceGuard guard(plan->device);

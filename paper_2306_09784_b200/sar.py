@@ -77,6 +77,8 @@ def load() -> ctypes.CDLL:
             lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
                                               P(ctypes.c_double * 3), _vp, _vp]
             lib.sar_doppler_table.restype = ctypes.c_int
+            lib.sar_image_sum.argtypes = [_vp, _vp, _i32, ctypes.c_int64, ctypes.c_int64, _vp]
+            lib.sar_image_sum.restype = ctypes.c_int
             lib.sar_plan_launch_count.argtypes = [_vp]
             lib.sar_plan_launch_count.restype = ctypes.c_int64
             lib.sar_destroy.argtypes = [_vp]
@@ -155,6 +157,22 @@ def doppler_table(radar, grid, q_ref, v_avg, device=0, out=None, stream=None):
     out = torch.empty((grid.ny, grid.nx), dtype=torch.float32, device=f"cuda:{device}") if out is None else out
     sar_doppler_table(radar_params(radar, 1, 1), grid_params(grid), q_ref, v_avg,
                       _dptr(out, torch.float32, (grid.ny, grid.nx), "doppler"), _stream_handle(stream))
+    return out
+
+
+def sar_image_sum(out_ptr, partials_ptr, n_partials, stride, n_elems, stream=0):
+    _check(load().sar_image_sum(out_ptr, partials_ptr, n_partials, stride, n_elems, stream))
+
+
+def image_sum(partials, out=None, stream=None):
+    """out = partials.sum(0) in k order, partials complex64 CUDA [n][...] (sar_image_sum)."""
+    import torch
+
+    n = partials.shape[0]
+    per = partials[0].numel()
+    out = torch.empty(partials.shape[1:], dtype=torch.complex64, device=partials.device) if out is None else out
+    sar_image_sum(_dptr(out, torch.complex64, tuple(partials.shape[1:]), "out"),
+                  _dptr(partials, torch.complex64, None, "partials"), n, per, per, _stream_handle(stream))
     return out
 
 

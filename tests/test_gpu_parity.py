@@ -344,6 +344,42 @@ def test_C5_streaming_frame_sampled_parity_and_chirp_shards(cuda_lib):
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
 
 
+def test_incremental_streaming_equals_one_shot_frame(cuda_lib):
+    """NEXT-2: with a world-fixed grid the frame after hop h is the sum of the last 8 per-hop
+    partial images; it equals one back-projection of the same 8192 chirps."""
+    import torch
+
+    from paper_2306_09784_b200.stream import IncrementalStream
+
+    scn = sarsim.make_config("C5", n_chirps=1024 * 11)
+    scn.grid = sarsim.Grid(-6.0, 4.0, 0.0, 0.01, 0.01, 600, 300)
+    raw = _raw(scn)
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    lo, hi = scn.antenna_box(1e-3)
+    st = IncrementalStream(scn.radar, scn.grid, scn.n_chirps, (lo, hi), hop=1024, hops_per_frame=8)
+    for _ in range(11):
+        frame = st.push(raw, tx)
+    ref_plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, 1, (lo, hi))
+    prof = ref_plan.range_compress(raw)
+    one = ref_plan.backproject(prof, tx, chirp0=3 * 1024, nchirp=8 * 1024)
+    torch.cuda.synchronize()
+    assert rel_err(frame.cpu().numpy(), one.cpu().numpy()) < 1e-5
+    st.close()
+    ref_plan.close()
+
+
+def test_image_sum_kernel(cuda_lib):
+    import torch
+
+    g = torch.Generator().manual_seed(0)
+    parts = torch.randn((5, 37, 41, 2), generator=g).to("cuda:0")
+    parts = torch.view_as_complex(parts.contiguous())
+    out = cuda_lib.image_sum(parts)
+    ref = parts[0] + parts[1] + parts[2] + parts[3] + parts[4]
+    torch.cuda.synchronize()
+    assert torch.allclose(out, ref, rtol=0, atol=1e-6)
+
+
 # ----------------------------------------------------------------------------- full-size configs
 @pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4"])
 def test_full_size_config_sampled_parity(cuda_lib, cfg):
