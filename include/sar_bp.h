@@ -76,6 +76,17 @@ typedef struct {
   int32_t nx, ny;
 } sar_grid_t;
 
+/* Polar reconstruction grid of Measure E: "a new grid ... that originates in
+ * the center of the synthetic aperture", range and azimuth spacing a factor finer than the
+ * PSF resolutions.  Pixel (i, j), i in [0, n_th) (bearing, fastest), j in [0, n_r) (range):
+ *   r_j = r0 + j dr,  th_i = th0 + i dth (radians from +y toward +x),
+ *   p = (xc + r_j sin th_i, yc + r_j cos th_i, zc).
+ * Images are row-major [n_r][n_th].  dr, dth > 0; r0 >= 0; n_th, n_r >= 1. */
+typedef struct {
+  double xc, yc, zc, r0, dr, th0, dth;
+  int32_t n_th, n_r;
+} sar_polar_grid_t;
+
 /* Declared axis-aligned bounding box of ALL antenna phase centres (TX and RX)
  * the plan will be used with.  The range crop is derived from it and the grid box
  * with the triangle inequality; positions outside it give wrong values (never an
@@ -111,6 +122,20 @@ sar_status_t sar_plan_geometry(const sar_radar_params_t* radar, const sar_grid_t
  * uploads them (synchronously, once).  *out receives the plan. */
 sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* grid,
                              const sar_box_t* antenna_box, int32_t device, sar_plan_t* out);
+
+/* Polar-grid plan (Measure E): as sar_plan_create, for a sar_polar_grid_t.  All other calls
+ * work unchanged on it, with "rows" = range rings j and "nx" = n_th bearings. */
+sar_status_t sar_plan_create_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                   const sar_box_t* antenna_box, int32_t device, sar_plan_t* out);
+sar_status_t sar_plan_geometry_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                     const sar_box_t* antenna_box, sar_plan_info_t* info);
+
+/* Resample a polar image onto a Cartesian grid "for comparability": bilinear
+ * interpolation of the complex values in (th, r) for each Cartesian pixel centre; pixels
+ * outside the polar coverage are 0.
+ *   polar_image dev complex [n_r][n_th] of `polar`; out dev complex [ny][nx] of `cart`. */
+sar_status_t sar_polar_to_cartesian(const sar_polar_grid_t* polar, const sar_complex64_t* polar_image,
+                                    const sar_grid_t* cart, sar_complex64_t* out, sar_stream_t stream);
 
 sar_status_t sar_plan_info(sar_plan_t plan, sar_plan_info_t* info);
 

@@ -15,6 +15,7 @@ Functions and the passages they follow (P:Lnnn = PAPER.md line):
   range_compress    H1, windowed zero-padded range FFT with centring ramp (A4-A8)
   backproject       H3-H5, Alg. 2 with Alg. 1 constants
   doppler_table     Measure D f_doppler(p) from the average velocity
+  polar_to_cartesian  Measure E polar image -> Cartesian grid, bilinear
 All are pinned by tests/test_oracle_pins.py (no function is "parity unpinned").
 """
 from __future__ import annotations
@@ -60,7 +61,9 @@ def _load():
             lib.oracle_backproject.argtypes = [P(d), i, i, i, i, d, d, d, d, i,
                                                P(d), P(d), P(d), P(d), i, i, P(d)]
             lib.oracle_doppler_table.argtypes = [d, d, i, P(d), i, P(d), P(d), d, P(d)]
+            lib.oracle_polar_to_cartesian.argtypes = [d, d, d, d, d, d, i, i, P(d), d, d, d, d, i, i, P(d)]
             for name in ("oracle_window", "oracle_dft_row", "oracle_fft", "oracle_doppler_table",
+                         "oracle_polar_to_cartesian",
                          "oracle_range_compress", "oracle_backproject", "oracle_version"):
                 getattr(lib, name).restype = ctypes.c_int
             _lib = lib
@@ -155,3 +158,19 @@ def doppler_table(radar, pixels, q_ref, v_avg, legs: float = 2.0) -> np.ndarray:
                                         _ptr(v, ctypes.c_double), float(legs), _ptr(out, ctypes.c_double)),
            "doppler_table")
     return out
+
+
+def polar_to_cartesian(polar, img, cart) -> np.ndarray:
+    """Polar image complex [n_r][n_th] of ``polar`` (xc, yc, r0, dr, th0, dth, n_th, n_r)
+    -> complex128 [ny][nx] on Cartesian grid ``cart`` (x0, y0, dx, dy, nx, ny)."""
+    img = np.asarray(img).reshape(polar.n_r, polar.n_th)
+    src = np.empty((polar.n_r, polar.n_th, 2), np.float64)
+    src[..., 0] = img.real
+    src[..., 1] = img.imag
+    out = np.empty((cart.ny, cart.nx, 2), np.float64)
+    _check(_load().oracle_polar_to_cartesian(
+        float(polar.xc), float(polar.yc), float(polar.r0), float(polar.dr), float(polar.th0), float(polar.dth),
+        int(polar.n_th), int(polar.n_r), _ptr(src, ctypes.c_double), float(cart.x0), float(cart.y0),
+        float(cart.dx), float(cart.dy), int(cart.nx), int(cart.ny), _ptr(out, ctypes.c_double)),
+        "polar_to_cartesian")
+    return out[..., 0] + 1j * out[..., 1]

@@ -21,6 +21,8 @@
  *   oracle_backproject     pinned (flat-profile closed form, exact-bin circular
  *                          track, point-target argmax and phase, permutation,
  *                          translation, linearity, brute-force numpy on tiny input)
+ *   oracle_polar_to_cartesian  pinned (node values reproduced, functions bilinear in
+ *                          (th, r) reproduced exactly, constant image, outside = 0)
  */
 #include <math.h>
 #include <pthread.h>
@@ -332,6 +334,43 @@ int oracle_doppler_table(double f0_hz, double fs_hz, int nfft, const double* pix
     const double r = sqrt(dx * dx + dy * dy + dz * dz);
     const double vr = r > 0.0 ? legs * (dx * v_avg[0] + dy * v_avg[1] + dz * v_avg[2]) / r : 0.0;
     out[p] = (f0_hz * vr / ORACLE_C_LIGHT) / (fs_hz / (double)nfft);
+  }
+  return 0;
+}
+
+/* Measure E image -> Cartesian grid "for comparability" (reading
+ * A18): for Cartesian pixel (x0 + ix dx, y0 + iy dy) take its polar coordinates about
+ * (xc, yc), r = |(x - xc, y - yc)|, th = atan2(x - xc, y - yc) (bearing from +y toward
+ * +x), and interpolate the polar image bilinearly in the fractional indices
+ * ((th - th0) / dth, (r - r0) / dr); pixels outside [0, n_th - 1] x [0, n_r - 1] are 0.
+ *   in  [n_r][n_th][2] (re, im);  out [ny][nx][2]. */
+int oracle_polar_to_cartesian(double xc, double yc, double r0, double dr, double th0, double dth,
+                              int n_th, int n_r, const double* in, double x0, double y0, double dx,
+                              double dy, int nx, int ny, double* out) {
+  if (!in || !out || n_th < 1 || n_r < 1 || nx < 0 || ny < 0 || !(dr > 0) || !(dth > 0)) return -1;
+  for (int iy = 0; iy < ny; ++iy) {
+    for (int ix = 0; ix < nx; ++ix) {
+      const double px = x0 + ix * dx - xc, py = y0 + iy * dy - yc;
+      const double fi = (atan2(px, py) - th0) / dth;
+      const double fj = (sqrt(px * px + py * py) - r0) / dr;
+      double re = 0.0, im = 0.0;
+      if (fi >= 0.0 && fj >= 0.0 && fi <= n_th - 1 && fj <= n_r - 1) {
+        int i0 = (int)floor(fi), j0 = (int)floor(fj);
+        if (i0 > n_th - 1) i0 = n_th - 1;
+        if (j0 > n_r - 1) j0 = n_r - 1;
+        const int i1 = i0 + 1 < n_th ? i0 + 1 : n_th - 1, j1 = j0 + 1 < n_r ? j0 + 1 : n_r - 1;
+        const double wi = fi - i0, wj = fj - j0;
+        const int idx[4][2] = {{j0, i0}, {j0, i1}, {j1, i0}, {j1, i1}};
+        const double w[4] = {(1 - wi) * (1 - wj), wi * (1 - wj), (1 - wi) * wj, wi * wj};
+        for (int c = 0; c < 4; ++c) {
+          const double* v = in + 2 * ((size_t)idx[c][0] * n_th + idx[c][1]);
+          re += w[c] * v[0];
+          im += w[c] * v[1];
+        }
+      }
+      out[2 * ((size_t)iy * nx + ix)] = re;
+      out[2 * ((size_t)iy * nx + ix) + 1] = im;
+    }
   }
   return 0;
 }

@@ -216,9 +216,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int i0 = tx * TX;               // first grid column of the tile
   const int j0 = ty * TY;               // first row of the tile, relative to row0
-  // tile anchor: centre of the full tile (even when ragged), fp64
-  const double PTx = a.x0 + (i0 + 0.5 * (TX - 1)) * a.dx;
-  const double PTy = a.y0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dy;
+  // tile anchor: centre of the full tile (even when ragged), fp64.  Cartesian grids:
+  // (x0 + i dx, y0 + j dy); polar grids (Measure E): (xc + r sin th, yc + r cos th).
+  double PTx, PTy;
+  if (a.polar) {
+    const double th = a.th0 + (i0 + 0.5 * (TX - 1)) * a.dth;
+    const double rr = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+    PTx = a.x0 + rr * sin(th);
+    PTy = a.y0 + rr * cos(th);
+  } else {
+    PTx = a.x0 + (i0 + 0.5 * (TX - 1)) * a.dx;
+    PTy = a.y0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dy;
+  }
   const double PTz = a.z0;
 
   if (threadIdx.x == 0) {
@@ -353,8 +362,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
     const int yl = (pi / kPatchesPerRow) * kPatchY + ly;
     gx[p] = i0 + xl;
     gy[p] = j0 + yl;
-    const double dux = (xl - 0.5 * (TX - 1)) * a.dx;
-    const double duy = (yl - 0.5 * (TY - 1)) * a.dy;
+    double dux, duy;
+    if (a.polar) {   // pixel offset from the anchor, both evaluated in fp64
+      const double th = a.th0 + (i0 + xl) * a.dth;
+      const double rr = a.r0 + (a.row0 + j0 + yl) * a.dr;
+      dux = (a.x0 + rr * sin(th)) - PTx;
+      duy = (a.y0 + rr * cos(th)) - PTy;
+    } else {
+      dux = (xl - 0.5 * (TX - 1)) * a.dx;
+      duy = (yl - 0.5 * (TY - 1)) * a.dy;
+    }
     ux[p] = (float)dux;
     uy[p] = (float)duy;
     wh[p] = (float)(dux * dux + duy * duy);   // |u|^2

@@ -47,6 +47,8 @@ struct BpArgs {
   int S;                   // ring stages (<= kBpMaxStages)
   int ncw, pb;             // CTA shape: consumer warps, pixels per consumer thread
   double x0, y0, z0, dx, dy;
+  int polar;               // 0: Cartesian (x0, y0, z0, dx, dy); 1: polar, centre (x0, y0, z0)
+  double r0, dr, th0, dth; // polar grid (Measure E)
   double a1, c2, k_lo;     // bins / metre two-way, cycles / metre two-way, crop start
   double kap_half;         // half window span in bins: 2 a1 rho + doppler bound
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
@@ -70,11 +72,24 @@ struct DopArgs {
 cudaError_t launch_doppler(const DopArgs& a, cudaStream_t s);
 cudaError_t launch_sum(float2* out, const float2* in, int n, long stride, long count, cudaStream_t s);
 
+// Polar -> Cartesian resampling arguments (resample_kernel.cu).
+struct ResampleArgs {
+  const float2* in;        // [n_r][n_th]
+  float2* out;             // [ny][nx]
+  double xc, yc, r0, dr, th0, dth;
+  int n_th, n_r;
+  double x0, y0, dx, dy;
+  int nx, ny;
+};
+cudaError_t launch_resample(const ResampleArgs& a, cudaStream_t s);
+
 }  // namespace sar
 
 struct sar_plan_s {
   sar_radar_params_t radar;
-  sar_grid_t grid;
+  sar_grid_t grid;          // Cartesian grid, or the stand-in (nx = n_th, ny = n_r) of a polar one
+  bool polar = false;
+  sar_polar_grid_t pgrid{};
   sar_box_t box;
   sar_plan_info_t info;
   int device;

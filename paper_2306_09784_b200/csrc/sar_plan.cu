@@ -49,9 +49,42 @@ struct Derived {
   int ncw, pb, stages;
 };
 
-// Host-side plan maths shared by sar_plan_geometry and sar_plan_create.
+// Polar grid (Measure E) -> bounding box of the annular sector and a Cartesian stand-in
+// (nx = n_th, ny = n_r) for the row/column bookkeeping shared with Cartesian plans.
+sar_status_t polar_box(const sar_polar_grid_t* pg, double lo[3], double hi[3], sar_grid_t* stand_in) {
+  if (!pg) return fail(SAR_ERR_INVALID_ARGUMENT, "null polar grid");
+  if (!finite_pos(pg->dr) || !finite_pos(pg->dth) || !(pg->r0 >= 0.0) || !isfinite(pg->r0) ||
+      !isfinite(pg->th0) || !isfinite(pg->xc) || !isfinite(pg->yc) || !isfinite(pg->zc) || pg->n_th < 1 ||
+      pg->n_r < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "polar grid needs r0 >= 0, dr, dth > 0, n_th, n_r >= 1");
+  const double th1 = pg->th0 + (pg->n_th - 1) * pg->dth;
+  if (th1 - pg->th0 >= 2.0 * sar::kPi) return fail(SAR_ERR_INVALID_ARGUMENT, "polar grid spans >= 2 pi");
+  const double r1 = pg->r0 + (pg->n_r - 1) * pg->dr;
+  lo[0] = lo[1] = 1e300;
+  hi[0] = hi[1] = -1e300;
+  auto add = [&](double rr, double th) {
+    const double x = pg->xc + rr * sin(th), y = pg->yc + rr * cos(th);
+    lo[0] = std::min(lo[0], x); hi[0] = std::max(hi[0], x);
+    lo[1] = std::min(lo[1], y); hi[1] = std::max(hi[1], y);
+  };
+  for (double rr : {pg->r0, r1}) {
+    add(rr, pg->th0);
+    add(rr, th1);
+    const int k0 = (int)floor(pg->th0 / (0.5 * sar::kPi)), k1 = (int)ceil(th1 / (0.5 * sar::kPi));
+    for (int k = k0; k <= k1; ++k) {  // bearings where sin or cos is extreme
+      const double t = k * 0.5 * sar::kPi;
+      if (t > pg->th0 && t < th1) add(rr, t);
+    }
+  }
+  lo[2] = hi[2] = pg->zc;
+  *stand_in = sar_grid_t{pg->xc, pg->yc, pg->zc, pg->dr, pg->dr, pg->n_th, pg->n_r};
+  return SAR_OK;
+}
+
+// Host-side plan maths shared by sar_plan_geometry and sar_plan_create (pg: polar grid or
+// nullptr; g then is the Cartesian stand-in from polar_box).
 sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_box_t* b,
-                    Derived* out) {
+                    Derived* out, const sar_polar_grid_t* pg = nullptr) {
   if (!r || !g || !b || !out) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
   if (!finite_pos(r->f0_hz) || !finite_pos(r->bandwidth_hz) || !finite_pos(r->chirp_s) ||
       !finite_pos(r->pri_s) || !finite_pos(r->sample_rate_hz))
@@ -82,8 +115,13 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   I.a1_bins_per_m = I.chirp_rate_hz_per_s * N / (sar::kLightSpeed * r->sample_rate_hz);
   I.c2_cycles_per_m = r->f0_hz / sar::kLightSpeed;                         // f0 / c (A3)
 
-  const double glo[3] = {g->x0, g->y0, g->z0};
-  const double ghi[3] = {g->x0 + (g->nx - 1) * g->dx, g->y0 + (g->ny - 1) * g->dy, g->z0};
+  double glo[3] = {g->x0, g->y0, g->z0};
+  double ghi[3] = {g->x0 + (g->nx - 1) * g->dx, g->y0 + (g->ny - 1) * g->dy, g->z0};
+  if (pg) {
+    sar_grid_t tmp;
+    sar_status_t st = polar_box(pg, glo, ghi, &tmp);
+    if (st != SAR_OK) return st;
+  }
   double dist_min, dist_max;
   box_distance(glo, ghi, b->lo, b->hi, &dist_min, &dist_max);
   I.d_min_m = 2.0 * dist_min;  // each leg lies in [dist_min, dist_max]
@@ -112,8 +150,24 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   out->pb = pb;
   I.tile_x = sar::kTileX;
   I.tile_y = ncw * pb;  // 32-pixel-wide rows of 8x4 patches: tile area = 32 * ncw * pb
-  const double hx = 0.5 * (I.tile_x - 1) * g->dx, hy = 0.5 * (I.tile_y - 1) * g->dy;
-  out->rho = sqrt(hx * hx + hy * hy) * (1.0 + 1e-9) + 1e-12;
+  if (!pg) {
+    const double hx = 0.5 * (I.tile_x - 1) * g->dx, hy = 0.5 * (I.tile_y - 1) * g->dy;
+    out->rho = sqrt(hx * hx + hy * hy) * (1.0 + 1e-9) + 1e-12;
+  } else {
+    // the tile of largest range is the widest: farthest corner from its anchor (the annular
+    // sector is convex in (r, th), its pixels lie within the corner distance)
+    const double ht = 0.5 * (I.tile_x - 1) * pg->dth, hr = 0.5 * (I.tile_y - 1) * pg->dr;
+    const int tiles_r = (pg->n_r + I.tile_y - 1) / I.tile_y;
+    const double rc = pg->r0 + ((tiles_r - 1) * I.tile_y + 0.5 * (I.tile_y - 1)) * pg->dr;
+    double rho = 0.0;
+    for (int sr = -1; sr <= 1; sr += 2)
+      for (int st2 = -1; st2 <= 1; st2 += 2) {
+        const double rr = rc + sr * hr, dt = st2 * ht;
+        const double dx = rr * sin(dt), dy = rr * cos(dt) - rc;
+        rho = std::max(rho, sqrt(dx * dx + dy * dy));
+      }
+    out->rho = rho * (1.0 + 1e-6) + 1e-9;
+  }
   const double kap_half = 2.0 * I.a1_bins_per_m * out->rho + dop;
   const double w = ceil(2.0 * kap_half) + 4.0;
   if (w > 4096.0)
@@ -121,12 +175,22 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
                 "pixel spacing too coarse: one BP tile spans more than 4096 range bins");
   I.window_bins = (int32_t)w;
   const bool bistatic = r->n_rx > 1;
-  if (cb <= 0) cb = std::max(1, 32 / r->n_rx);
-  const size_t stage_bytes = sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, 1, bistatic) - 16 * sar::kBpMaxStages;
-  if (stages <= 0) stages = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
-  stages = std::max(2, std::min(sar::kBpMaxStages, stages));
-  if (sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, stages, bistatic) > 200 * 1024)
-    return fail(SAR_ERR_INVALID_ARGUMENT, "BP shared-memory ring does not fit (window too wide)");
+  const bool auto_cb = cb <= 0, auto_stages = stages <= 0;
+  if (auto_cb) cb = std::max(1, 32 / r->n_rx);
+  for (;;) {
+    const size_t stage_bytes = sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, 1, bistatic) - 16 * sar::kBpMaxStages;
+    int st = stages;
+    if (auto_stages) st = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
+    st = std::max(2, std::min(sar::kBpMaxStages, st));
+    // coarse grids (wide windows): fewer chirps per stage until the ring fits
+    if (sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, st, bistatic) <= 200 * 1024) {
+      stages = st;
+      break;
+    }
+    if (!auto_cb || cb == 1)
+      return fail(SAR_ERR_INVALID_ARGUMENT, "BP shared-memory ring does not fit (window too wide)");
+    cb = std::max(1, cb / 2);
+  }
   I.chirps_per_stage = cb;
   out->stages = stages;
   if ((int64_t)r->n_chirps * r->n_rx * (I.n_bins + 1) >= (int64_t)1 << 31)
@@ -191,12 +255,47 @@ sar_status_t sar_plan_geometry(const sar_radar_params_t* radar, const sar_grid_t
   return SAR_OK;
 }
 
+sar_status_t sar_plan_geometry_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                     const sar_box_t* antenna_box, sar_plan_info_t* info) {
+  if (!info) return fail(SAR_ERR_INVALID_ARGUMENT, "info is null");
+  sar_grid_t stand_in;
+  double lo[3], hi[3];
+  sar_status_t st = polar_box(grid, lo, hi, &stand_in);
+  if (st != SAR_OK) return st;
+  Derived d;
+  st = derive(radar, &stand_in, antenna_box, &d, grid);
+  if (st != SAR_OK) return st;
+  *info = d.info;
+  return SAR_OK;
+}
+
+static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                                const sar_box_t* antenna_box, int32_t device, sar_plan_t* out,
+                                const sar_polar_grid_t* pg);
+
 sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* grid,
                              const sar_box_t* antenna_box, int32_t device, sar_plan_t* out) {
+  return create_impl(radar, grid, antenna_box, device, out, nullptr);
+}
+
+sar_status_t sar_plan_create_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                   const sar_box_t* antenna_box, int32_t device, sar_plan_t* out) {
+  if (!out) return fail(SAR_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  sar_grid_t stand_in;
+  double lo[3], hi[3];
+  sar_status_t st = polar_box(grid, lo, hi, &stand_in);
+  if (st != SAR_OK) return st;
+  return create_impl(radar, &stand_in, antenna_box, device, out, grid);
+}
+
+static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_t* grid,
+                                const sar_box_t* antenna_box, int32_t device, sar_plan_t* out,
+                                const sar_polar_grid_t* pg) {
   if (!out) return fail(SAR_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   Derived d;
-  sar_status_t st = derive(radar, grid, antenna_box, &d);
+  sar_status_t st = derive(radar, grid, antenna_box, &d, pg);
   if (st != SAR_OK) return st;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -217,6 +316,8 @@ sar_status_t sar_plan_create(const sar_radar_params_t* radar, const sar_grid_t* 
   if (!p) return fail(SAR_ERR_NO_MEMORY, "host allocation failed");
   p->radar = *radar;
   p->grid = *grid;
+  p->polar = pg != nullptr;
+  if (pg) p->pgrid = *pg;
   p->box = *antenna_box;
   p->info = d.info;
   p->device = device;
@@ -369,6 +470,11 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
   a.z0 = g.z0;
   a.dx = g.dx;
   a.dy = g.dy;
+  a.polar = plan->polar ? 1 : 0;
+  a.r0 = plan->pgrid.r0;
+  a.dr = plan->pgrid.dr;
+  a.th0 = plan->pgrid.th0;
+  a.dth = plan->pgrid.dth;
   a.a1 = plan->info.a1_bins_per_m;
   a.c2 = plan->info.c2_cycles_per_m;
   a.k_lo = plan->info.k_lo;
@@ -475,6 +581,37 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
   a.bins_per_mps = radar->f0_hz / sar::kLightSpeed / (radar->sample_rate_hz / radar->fft_len);
   cudaError_t e = sar::launch_doppler(a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "doppler table launch");
+  return SAR_OK;
+}
+
+sar_status_t sar_polar_to_cartesian(const sar_polar_grid_t* polar, const sar_complex64_t* polar_image,
+                                    const sar_grid_t* cart, sar_complex64_t* out, sar_stream_t stream) {
+  if (!polar || !polar_image || !cart || !out) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  double lo[3], hi[3];
+  sar_grid_t stand_in;
+  sar_status_t st = polar_box(polar, lo, hi, &stand_in);
+  if (st != SAR_OK) return st;
+  if (!finite_pos(cart->dx) || !finite_pos(cart->dy) || cart->nx < 1 || cart->ny < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "Cartesian grid needs dx, dy > 0 and nx, ny >= 1");
+  sar::ResampleArgs a;
+  a.in = reinterpret_cast<const float2*>(polar_image);
+  a.out = reinterpret_cast<float2*>(out);
+  a.xc = polar->xc;
+  a.yc = polar->yc;
+  a.r0 = polar->r0;
+  a.dr = polar->dr;
+  a.th0 = polar->th0;
+  a.dth = polar->dth;
+  a.n_th = polar->n_th;
+  a.n_r = polar->n_r;
+  a.x0 = cart->x0;
+  a.y0 = cart->y0;
+  a.dx = cart->dx;
+  a.dy = cart->dy;
+  a.nx = cart->nx;
+  a.ny = cart->ny;
+  cudaError_t e = sar::launch_resample(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "polar-to-Cartesian launch");
   return SAR_OK;
 }
 

@@ -37,6 +37,12 @@ class Grid(ctypes.Structure):
                 ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32)]
 
 
+class PolarGrid(ctypes.Structure):
+    _fields_ = [("xc", ctypes.c_double), ("yc", ctypes.c_double), ("zc", ctypes.c_double), ("r0", ctypes.c_double),
+                ("dr", ctypes.c_double), ("th0", ctypes.c_double), ("dth", ctypes.c_double),
+                ("n_th", ctypes.c_int32), ("n_r", ctypes.c_int32)]
+
+
 class Box(ctypes.Structure):
     _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3)]
 
@@ -77,6 +83,11 @@ def load() -> ctypes.CDLL:
             lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
                                               P(ctypes.c_double * 3), _vp, _vp]
             lib.sar_doppler_table.restype = ctypes.c_int
+            lib.sar_plan_create_polar.argtypes = [P(RadarParams), P(PolarGrid), P(Box), _i32, P(_vp)]
+            lib.sar_plan_geometry_polar.argtypes = [P(RadarParams), P(PolarGrid), P(Box), P(PlanInfo)]
+            lib.sar_polar_to_cartesian.argtypes = [P(PolarGrid), _vp, P(Grid), _vp, _vp]
+            for n in ("sar_plan_create_polar", "sar_plan_geometry_polar", "sar_polar_to_cartesian"):
+                getattr(lib, n).restype = ctypes.c_int
             lib.sar_image_sum.argtypes = [_vp, _vp, _i32, ctypes.c_int64, ctypes.c_int64, _vp]
             lib.sar_image_sum.restype = ctypes.c_int
             lib.sar_plan_launch_count.argtypes = [_vp]
@@ -107,6 +118,41 @@ def sar_plan_create(radar: RadarParams, grid: Grid, box: Box, device: int = 0) -
     h = _vp()
     _check(load().sar_plan_create(ctypes.byref(radar), ctypes.byref(grid), ctypes.byref(box), device, ctypes.byref(h)))
     return h.value
+
+
+def sar_plan_create_polar(radar: RadarParams, grid: PolarGrid, box: Box, device: int = 0) -> int:
+    h = _vp()
+    _check(load().sar_plan_create_polar(ctypes.byref(radar), ctypes.byref(grid), ctypes.byref(box), device,
+                                        ctypes.byref(h)))
+    return h.value
+
+
+def sar_plan_geometry_polar(radar: RadarParams, grid: PolarGrid, box: Box) -> PlanInfo:
+    info = PlanInfo()
+    _check(load().sar_plan_geometry_polar(ctypes.byref(radar), ctypes.byref(grid), ctypes.byref(box),
+                                          ctypes.byref(info)))
+    return info
+
+
+def sar_polar_to_cartesian(polar: PolarGrid, polar_ptr, cart: Grid, out_ptr, stream=0):
+    _check(load().sar_polar_to_cartesian(ctypes.byref(polar), polar_ptr, ctypes.byref(cart), out_ptr, stream))
+
+
+def polar_grid_params(g) -> PolarGrid:
+    return PolarGrid(g.xc, g.yc, g.zc, g.r0, g.dr, g.th0, g.dth, g.n_th, g.n_r)
+
+
+def polar_to_cartesian(polar_grid, polar_img, cart_grid, out=None, stream=None):
+    """Bilinear (bearing, range) resampling of a polar image onto a Cartesian grid."""
+    import torch
+
+    out = torch.empty((cart_grid.ny, cart_grid.nx), dtype=torch.complex64, device=polar_img.device) \
+        if out is None else out
+    sar_polar_to_cartesian(polar_grid_params(polar_grid),
+                           _dptr(polar_img, torch.complex64, (polar_grid.n_r, polar_grid.n_th), "polar image"),
+                           grid_params(cart_grid), _dptr(out, torch.complex64, (cart_grid.ny, cart_grid.nx), "out"),
+                           _stream_handle(stream))
+    return out
 
 
 def sar_plan_info(plan: int) -> PlanInfo:
@@ -254,9 +300,14 @@ class Plan:
         self.n_rx = n_rx
         self.device = device
         self._rp = radar_params(radar, n_chirps, n_rx, doppler_max_bins)
-        self._gp = grid_params(grid)
         self._bp = box_params(*antenna_box)
-        self.handle = sar_plan_create(self._rp, self._gp, self._bp, device)
+        self.polar = hasattr(grid, "n_th")     # a polar grid (sarsim.PolarGrid): image [n_r][n_th]
+        if self.polar:
+            self._gp = polar_grid_params(grid)
+            self.handle = sar_plan_create_polar(self._rp, self._gp, self._bp, device)
+        else:
+            self._gp = grid_params(grid)
+            self.handle = sar_plan_create(self._rp, self._gp, self._bp, device)
         self.info = sar_plan_info(self.handle)
         self.k_lo, self.n_bins = self.info.k_lo, self.info.n_bins
 

@@ -1,0 +1,146 @@
+"""Polar reconstruction grid (Measure E; NEXT-1) on CPU: the oracle's
+polar -> Cartesian resampling pinned against bilinear invariants, the polar pixel
+generator against its definition, the grid recipe against the resolution formulas, and
+the C ABI's host-side polar plan maths (no device needed)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import sarsim
+from paper_2306_09784_b200 import _build, sar
+from sarsim import C_LIGHT, Grid, PolarGrid, Radar
+
+PG = PolarGrid(0.3, -0.2, 0.0, 4.0, 0.05, -0.4, 0.01, 81, 31)
+
+
+def _one_pixel_grid(x, y):
+    return Grid(x, y, 0.0, 1.0, 1.0, 1, 1)
+
+
+def _bilinear(fi, fj):
+    """A function bilinear in the fractional polar indices (i: bearing, j: range)."""
+    return (0.7 - 0.2j) + (0.03 + 0.01j) * fi + (-0.05 + 0.02j) * fj + (0.002 - 0.004j) * fi * fj
+
+
+def _polar_image(f):
+    jj, ii = np.meshgrid(np.arange(PG.n_r), np.arange(PG.n_th), indexing="ij")
+    return f(ii.astype(float), jj.astype(float))
+
+
+def test_polar_pixels_follow_the_definition():
+    pix = PG.pixels().reshape(PG.n_r, PG.n_th, 3)
+    d = pix[..., :2] - np.array([PG.xc, PG.yc])
+    r = np.hypot(d[..., 0], d[..., 1])
+    assert np.allclose(r, (PG.r0 + PG.dr * np.arange(PG.n_r))[:, None], atol=1e-12)
+    # bearing measured from +y toward +x: a pixel at th = 0 is straight ahead (+y)
+    th = np.arctan2(d[..., 0], d[..., 1])
+    assert np.allclose(th, (PG.th0 + PG.dth * np.arange(PG.n_th))[None, :], atol=1e-12)
+    assert np.allclose(PG.pixel_list(np.array([[3, 5]])), pix[3, 5])
+    assert PG.nx == PG.n_th and PG.ny == PG.n_r
+
+
+def test_resample_reproduces_bilinear_functions_exactly():
+    """Bilinear interpolation is exact for functions bilinear in (th, r): probe points are
+    placed by the FORWARD polar map at known fractional indices."""
+    img = _polar_image(_bilinear)
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        fi = rng.uniform(0, PG.n_th - 1)
+        fj = rng.uniform(0, PG.n_r - 1)
+        r = PG.r0 + fj * PG.dr
+        th = PG.th0 + fi * PG.dth
+        cart = _one_pixel_grid(PG.xc + r * math.sin(th), PG.yc + r * math.cos(th))
+        got = oracle.polar_to_cartesian(PG, img, cart)[0, 0]
+        assert abs(got - _bilinear(fi, fj)) < 1e-9
+
+
+def test_resample_nodes_constant_and_outside():
+    img = _polar_image(_bilinear)
+    for (j, i) in [(0, 0), (PG.n_r - 1, PG.n_th - 1), (7, 40), (30, 3)]:
+        x, y, _ = PG.pixel_list(np.array([[j, i]]))[0]
+        got = oracle.polar_to_cartesian(PG, img, _one_pixel_grid(x, y))[0, 0]
+        assert abs(got - img[j, i]) < 1e-9
+    # a constant polar image resamples to the constant inside the sector, 0 outside
+    const = np.full((PG.n_r, PG.n_th), 2.0 - 1.0j)
+    cart = Grid(-2.5, 2.0, 0.0, 0.05, 0.05, 120, 90)
+    out = oracle.polar_to_cartesian(PG, const, cart)
+    pix = cart.pixels().reshape(cart.ny, cart.nx, 3)
+    d = pix[..., :2] - np.array([PG.xc, PG.yc])
+    r = np.hypot(d[..., 0], d[..., 1])
+    th = np.arctan2(d[..., 0], d[..., 1])
+    inside = (r >= PG.r0 + 1e-9) & (r <= PG.r0 + (PG.n_r - 1) * PG.dr - 1e-9) & \
+             (th >= PG.th0 + 1e-9) & (th <= PG.th0 + (PG.n_th - 1) * PG.dth - 1e-9)
+    outside = (r < PG.r0 - 1e-9) | (r > PG.r0 + (PG.n_r - 1) * PG.dr + 1e-9) | \
+              (th < PG.th0 - 1e-9) | (th > PG.th0 + (PG.n_th - 1) * PG.dth + 1e-9)
+    assert inside.sum() > 1000 and outside.sum() > 1000
+    assert np.allclose(out[inside], 2.0 - 1.0j, atol=1e-12)
+    assert np.all(out[outside] == 0)
+
+
+def test_polar_oracle_image_peaks_on_target_node():
+    scn = sarsim.polar_small_config(n_chirps=48, n_th=50, n_r=24, seed=33)
+    r = scn.radar
+    for k, (j, i) in enumerate(scn.isolated):    # one target at a time: a single PSF per image
+        raw = sarsim.simulate_raw(scn, targets=scn.targets[k:k + 1], amps=scn.amps[k:k + 1]).numpy()
+        prof = oracle.range_compress(raw, r.fft_len, r.range_window, scn.wsar)
+        img = oracle.backproject(prof, 0, r, scn.tx, None, scn.grid.pixels()).reshape(24, 50)
+        assert np.unravel_index(np.argmax(np.abs(img)), img.shape) == (j, i)
+        # coherent gain and phase at the target (A2): sum over chirps of |a| e^{j arg a}
+        assert abs(img[j, i] - scn.amps[k] * scn.n_chirps) < 0.01 * abs(scn.amps[k]) * scn.n_chirps
+
+
+def test_polar_recipe_spacing():
+    """dr = (c / 2B) / f and r_max dth = lambda r_max / (2 L f)."""
+    r = Radar()
+    L = 0.30
+    g = sarsim.polar_recipe(r, (0, 0, 0), L, 1.0, 10.0, -0.6, 0.6, factor=2.5)
+    assert math.isclose(g.dr, C_LIGHT / (2 * r.bandwidth_hz) / 2.5)
+    assert math.isclose(g.dth, r.wavelength_m / (2 * L * 2.5))
+    assert g.r0 + (g.n_r - 1) * g.dr <= 10.0 < g.r0 + g.n_r * g.dr
+    assert g.th0 + (g.n_th - 1) * g.dth <= 0.6 < g.th0 + g.n_th * g.dth
+    with pytest.raises(ValueError):
+        sarsim.polar_recipe(r, (0, 0, 0), L, 1.0, 10.0, -0.6, 0.6, factor=1.5)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return sar.load()
+
+
+def _polar_params(scn):
+    rp = sar.radar_params(scn.radar, scn.n_chirps, scn.n_rx)
+    lo, hi = scn.antenna_box(1e-3)
+    return rp, sar.polar_grid_params(scn.grid), sar.box_params(lo, hi)
+
+
+@pytest.mark.parametrize("th0", [-0.18, 2.9, -7.0])
+def test_polar_plan_geometry_crop_covers_every_path(lib, th0):
+    scn = sarsim.polar_small_config(n_chirps=40, th0=th0, dth=0.01, n_th=70, n_r=40, curved=True)
+    rp, gp, bp = _polar_params(scn)
+    info = sar.sar_plan_geometry_polar(rp, gp, bp)
+    pix = scn.grid.pixels()
+    d = 2 * np.linalg.norm(pix[:, None, :] - scn.tx[None, :, :], axis=2)
+    assert info.k_lo <= math.floor(info.a1_bins_per_m * d.min())
+    assert info.k_lo + info.n_bins - 1 >= math.floor(info.a1_bins_per_m * d.max()) + 1
+    assert info.updates_per_image == 70 * 40 * 40
+    # a tile spans 32 bearings x tile_y ranges: its half-diagonal bounds the window
+    rmax = scn.grid.r0 + (scn.grid.n_r - 1) * scn.grid.dr
+    rho_lo = 0.5 * math.hypot(31 * scn.grid.dth * scn.grid.r0, (info.tile_y - 1) * scn.grid.dr)
+    assert info.window_bins >= 4 * info.a1_bins_per_m * rho_lo
+    assert info.window_bins <= 4 * info.a1_bins_per_m * 0.5 * math.hypot(
+        32 * scn.grid.dth * rmax, info.tile_y * scn.grid.dr) * 1.01 + 8
+
+
+def test_polar_plan_geometry_rejects_bad_grids(lib):
+    scn = sarsim.polar_small_config(n_chirps=8)
+    for kw in [dict(dth=0.0), dict(dr=-0.1), dict(r0=-1.0), dict(n_th=0), dict(n_r=0),
+               dict(dth=2 * math.pi / 10, n_th=11), dict(dr=float("nan"))]:
+        rp, gp, bp = _polar_params(scn)
+        for k, v in kw.items():
+            setattr(gp, k, v)
+        with pytest.raises(sar.SarError) as e:
+            sar.sar_plan_geometry_polar(rp, gp, bp)
+        assert e.value.status == 1, kw
