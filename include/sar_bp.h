@@ -109,6 +109,10 @@ typedef struct {
   int32_t window_bins;        /* profile bins staged per (tile, chirp, rx) */
   int32_t chirps_per_stage;   /* chirps per shared-memory ring stage */
   int64_t updates_per_image;  /* nx * ny * n_chirps * n_rx */
+  double window_half_bins;    /* bound on |kappa(p) - kappa(anchor)| over a tile (bins,
+                                 incl. the Doppler bound); the staged window is
+                                 [floor(kappa_anchor - half) - 1, + window_bins) */
+  double tile_rho_m;          /* largest tile half-diagonal (m) */
 } sar_plan_info_t;
 
 /* Validate parameters and compute the derived quantities without touching a GPU.

@@ -38,6 +38,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "sar_internal.h"
 
@@ -196,7 +197,9 @@ __host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bo
   return L;
 }
 
-template <bool BISTATIC, bool DOP, bool SAFE, int NCW, int PB>
+// NEAR: the plan has tiles within 3 rho of the antenna box; those tiles (a per-CTA,
+// warp-uniform decision) take the near-field SAFE consumer path, all others the fast one.
+template <bool BISTATIC, bool DOP, bool NEAR, int NCW, int PB>
 __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   constexpr int TX = kTileX;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
           const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
-          srec[2 * c + 1] = make_float4(SAFE ? (float)(Dz * Dz) : 0.f, 0.f, 0.f, 0.f);
+          srec[2 * c + 1] = make_float4(NEAR ? (float)(Dz * Dz) : 0.f, 0.f, 0.f, 0.f);
         }
       }
       for (int e = lane; e < items; e += 32) {
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
         const uint32_t off = waddr + 16u * (uint32_t)wh - 16u * kMagicBits;
         const int ri = BISTATIC ? a.CB + e : e;
         srec[2 * ri] = leg0;
-        srec[2 * ri + 1] = make_float4(SAFE ? (float)(dz * dz) : 0.f,
+        srec[2 * ri + 1] = make_float4(NEAR ? (float)(dz * dz) : 0.f,
                                        (float)(kap - k0 - 0.5 - wh), 0.f, __uint_as_float(off));
         skw[e] = make_int2(k0, (m * a.n_rx + n) * a.n_bins);
       }
@@ -351,6 +354,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   }
 
   // ============================== CONSUMERS ==============================
+  auto consume = [&](auto safe_tag) {
+  constexpr bool SAFE = decltype(safe_tag)::value;
   const int lx = lane & (kPatchX - 1), ly = lane >> 3;
   constexpr int kPatchesPerRow = TX / kPatchX;
   float ux[PB], uy[PB], wh[PB], acc_r[PB], acc_i[PB], fd[PB];
@@ -554,6 +559,21 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       }
     }
   }
+  };
+  if constexpr (NEAR) {
+    // near-field test of this tile: distance from the anchor to the antenna box
+    double d2 = 0.0;
+    const double pt[3] = {PTx, PTy, PTz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double gap = fmax(0.0, fmax(a.box_lo[k] - pt[k], pt[k] - a.box_hi[k]));
+      d2 += gap * gap;
+    }
+    if (d2 < a.near_r * a.near_r) consume(std::true_type{});
+    else consume(std::false_type{});
+  } else {
+    consume(std::false_type{});
+  }
 }
 
 template <bool BI, bool DOP, bool SAFE, int NCW, int PB>
@@ -594,13 +614,13 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
 }
 
 template <int NCW, int PB>
-cudaError_t launch_shape(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s) {
+cudaError_t launch_shape(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
   if (bistatic) {
-    if (doppler) return safe ? launch_one<true, true, true, NCW, PB>(a, s) : launch_one<true, true, false, NCW, PB>(a, s);
-    return safe ? launch_one<true, false, true, NCW, PB>(a, s) : launch_one<true, false, false, NCW, PB>(a, s);
+    if (doppler) return near ? launch_one<true, true, true, NCW, PB>(a, s) : launch_one<true, true, false, NCW, PB>(a, s);
+    return near ? launch_one<true, false, true, NCW, PB>(a, s) : launch_one<true, false, false, NCW, PB>(a, s);
   }
-  if (doppler) return safe ? launch_one<false, true, true, NCW, PB>(a, s) : launch_one<false, true, false, NCW, PB>(a, s);
-  return safe ? launch_one<false, false, true, NCW, PB>(a, s) : launch_one<false, false, false, NCW, PB>(a, s);
+  if (doppler) return near ? launch_one<false, true, true, NCW, PB>(a, s) : launch_one<false, true, false, NCW, PB>(a, s);
+  return near ? launch_one<false, false, true, NCW, PB>(a, s) : launch_one<false, false, false, NCW, PB>(a, s);
 }
 
 }  // namespace
@@ -614,11 +634,11 @@ size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic) {
   return make_layout(W, CB, n_rx, S, bistatic).total;
 }
 
-cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s) {
-  if (a.ncw == 8 && a.pb == 4) return launch_shape<8, 4>(a, bistatic, doppler, safe, s);
-  if (a.ncw == 4 && a.pb == 8) return launch_shape<4, 8>(a, bistatic, doppler, safe, s);
-  if (a.ncw == 4 && a.pb == 4) return launch_shape<4, 4>(a, bistatic, doppler, safe, s);
-  if (a.ncw == 8 && a.pb == 8) return launch_shape<8, 8>(a, bistatic, doppler, safe, s);
+cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
+  if (a.ncw == 8 && a.pb == 4) return launch_shape<8, 4>(a, bistatic, doppler, near, s);
+  if (a.ncw == 4 && a.pb == 8) return launch_shape<4, 8>(a, bistatic, doppler, near, s);
+  if (a.ncw == 4 && a.pb == 4) return launch_shape<4, 4>(a, bistatic, doppler, near, s);
+  if (a.ncw == 8 && a.pb == 8) return launch_shape<8, 8>(a, bistatic, doppler, near, s);
   return cudaErrorInvalidConfiguration;
 }
 

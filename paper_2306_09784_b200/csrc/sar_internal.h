@@ -50,7 +50,9 @@ struct BpArgs {
   int polar;               // 0: Cartesian (x0, y0, z0, dx, dy); 1: polar, centre (x0, y0, z0)
   double r0, dr, th0, dth; // polar grid (Measure E)
   double a1, c2, k_lo;     // bins / metre two-way, cycles / metre two-way, crop start
-  double kap_half;         // half window span in bins: 2 a1 rho + doppler bound
+  double kap_half;         // half window span in bins: 2 a1 rho_win + doppler bound
+  double box_lo[3], box_hi[3];  // declared antenna box (near-field tile test)
+  double near_r;           // tiles whose anchor lies within near_r of the box run the SAFE form
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };
@@ -58,7 +60,7 @@ struct BpArgs {
 bool bp_shape_supported(int ncw, int pb);
 size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
-cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool safe, cudaStream_t s);
+cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s);
 
 // Doppler-table kernel arguments (doppler_kernel.cu).
 struct DopArgs {
@@ -95,7 +97,8 @@ struct sar_plan_s {
   int device;
   bool near_field;         // an antenna may come within 2 rho of a tile anchor
   int bp_ncw, bp_pb, bp_stages;
-  double tile_rho;         // tile half-diagonal (m)
+  double tile_rho;         // tile half-diagonal (m), max over tiles
+  double win_rho;          // per-leg half spread of |p - q| over a tile (m): sets kap_half
   float rc_scale;
   float* d_window = nullptr;
   float2* d_twiddle = nullptr;

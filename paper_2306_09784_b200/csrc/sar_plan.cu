@@ -44,7 +44,8 @@ void box_distance(const double alo[3], const double ahi[3], const double blo[3],
 
 struct Derived {
   sar_plan_info_t info;
-  double rho;
+  double rho;       // tile half-diagonal, max over tiles (near-field test)
+  double win_rho;   // per-leg half spread of |p - q| over a tile, max over tiles (window)
   bool near_field;
   int ncw, pb, stages;
 };
@@ -153,27 +154,48 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   if (!pg) {
     const double hx = 0.5 * (I.tile_x - 1) * g->dx, hy = 0.5 * (I.tile_y - 1) * g->dy;
     out->rho = sqrt(hx * hx + hy * hy) * (1.0 + 1e-9) + 1e-12;
+    out->win_rho = out->rho;   // triangle inequality: ||p - q| - |P_T - q|| <= |p - P_T|
   } else {
-    // the tile of largest range is the widest: farthest corner from its anchor (the annular
-    // sector is convex in (r, th), its pixels lie within the corner distance)
+    // Per tile row (anchor radius rc, half extents hr in range and ht in bearing):
+    //  * rho_T: farthest tile corner from the anchor (the annular patch lies within it);
+    //  * window: the triangle bound rho_T is loose for polar tiles seen from near the polar
+    //    centre c.  With s = q - c (horizontal part s_h), |d|p - q|/dr| <= 1 and
+    //    |d|p - q|/dth| = r |s_h . e_perp| / |p - q| <= r s_h / (r - s_h), so moving from the
+    //    anchor first in range, then in bearing at radius r >= r_in = rc - hr gives
+    //    ||p - q| - |P_T - q|| <= hr + ht r_in s_h / (r_in - s_h) when r_in > s_h.
     const double ht = 0.5 * (I.tile_x - 1) * pg->dth, hr = 0.5 * (I.tile_y - 1) * pg->dr;
     const int tiles_r = (pg->n_r + I.tile_y - 1) / I.tile_y;
-    const double rc = pg->r0 + ((tiles_r - 1) * I.tile_y + 0.5 * (I.tile_y - 1)) * pg->dr;
-    double rho = 0.0;
-    for (int sr = -1; sr <= 1; sr += 2)
-      for (int st2 = -1; st2 <= 1; st2 += 2) {
-        const double rr = rc + sr * hr, dt = st2 * ht;
-        const double dx = rr * sin(dt), dy = rr * cos(dt) - rc;
-        rho = std::max(rho, sqrt(dx * dx + dy * dy));
-      }
+    double sh = 0.0;
+    for (int cx = 0; cx < 2; ++cx)
+      for (int cy = 0; cy < 2; ++cy)
+        sh = std::max(sh, hypot((cx ? b->hi[0] : b->lo[0]) - pg->xc, (cy ? b->hi[1] : b->lo[1]) - pg->yc));
+    double rho = 0.0, wrho = 0.0;
+    for (int t = 0; t < tiles_r; ++t) {
+      const double rc = pg->r0 + (t * I.tile_y + 0.5 * (I.tile_y - 1)) * pg->dr;
+      double rho_t = 0.0;
+      for (int sr = -1; sr <= 1; sr += 2)
+        for (int st2 = -1; st2 <= 1; st2 += 2) {
+          const double rr = rc + sr * hr, dt = st2 * ht;
+          const double dx = rr * sin(dt), dy = rr * cos(dt) - rc;
+          rho_t = std::max(rho_t, sqrt(dx * dx + dy * dy));
+        }
+      double w_t = rho_t;
+      const double r_in = rc - hr;
+      if (r_in > sh * (1.0 + 1e-9)) w_t = std::min(w_t, hr + ht * r_in * sh / (r_in - sh));
+      rho = std::max(rho, rho_t);
+      wrho = std::max(wrho, w_t);
+    }
     out->rho = rho * (1.0 + 1e-6) + 1e-9;
+    out->win_rho = wrho * (1.0 + 1e-6) + 1e-9;
   }
-  const double kap_half = 2.0 * I.a1_bins_per_m * out->rho + dop;
+  const double kap_half = 2.0 * I.a1_bins_per_m * out->win_rho + dop;
   const double w = ceil(2.0 * kap_half) + 4.0;
   if (w > 4096.0)
     return fail(SAR_ERR_INVALID_ARGUMENT,
                 "pixel spacing too coarse: one BP tile spans more than 4096 range bins");
   I.window_bins = (int32_t)w;
+  I.window_half_bins = kap_half;
+  I.tile_rho_m = out->rho;
   const bool bistatic = r->n_rx > 1;
   const bool auto_cb = cb <= 0, auto_stages = stages <= 0;
   if (auto_cb) cb = std::max(1, 32 / r->n_rx);
@@ -323,6 +345,7 @@ static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_
   p->device = device;
   p->near_field = d.near_field;
   p->tile_rho = d.rho;
+  p->win_rho = d.win_rho;
   p->bp_ncw = d.ncw;
   p->bp_pb = d.pb;
   p->bp_stages = d.stages;
@@ -478,7 +501,12 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
   a.a1 = plan->info.a1_bins_per_m;
   a.c2 = plan->info.c2_cycles_per_m;
   a.k_lo = plan->info.k_lo;
-  a.kap_half = 2.0 * a.a1 * plan->tile_rho + (double)r.doppler_max_bins;
+  a.kap_half = plan->info.window_half_bins;
+  for (int k = 0; k < 3; ++k) {
+    a.box_lo[k] = plan->box.lo[k];
+    a.box_hi[k] = plan->box.hi[k];
+  }
+  a.near_r = 3.0 * plan->tile_rho + 1e-3;
   const bool bistatic = rx_pos != nullptr;
   a.A1f = (float)(bistatic ? a.a1 : 2.0 * a.a1);
   a.binphase = plan->d_binphase;

@@ -52,7 +52,8 @@ class PlanInfo(ctypes.Structure):
                 ("c2_cycles_per_m", ctypes.c_double), ("d_min_m", ctypes.c_double), ("d_max_m", ctypes.c_double),
                 ("k_lo", ctypes.c_int32), ("n_bins", ctypes.c_int32), ("tile_x", ctypes.c_int32),
                 ("tile_y", ctypes.c_int32), ("window_bins", ctypes.c_int32), ("chirps_per_stage", ctypes.c_int32),
-                ("updates_per_image", ctypes.c_int64)]
+                ("updates_per_image", ctypes.c_int64), ("window_half_bins", ctypes.c_double),
+                ("tile_rho_m", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -118,20 +118,46 @@ def _polar_params(scn):
 
 @pytest.mark.parametrize("th0", [-0.18, 2.9, -7.0])
 def test_polar_plan_geometry_crop_covers_every_path(lib, th0):
-    scn = sarsim.polar_small_config(n_chirps=40, th0=th0, dth=0.01, n_th=70, n_r=40, curved=True)
+    _check_crop_and_window(sarsim.polar_small_config(n_chirps=40, th0=th0, dth=0.01, n_th=70, n_r=40, curved=True))
+
+
+def _check_crop_and_window(scn):
     rp, gp, bp = _polar_params(scn)
     info = sar.sar_plan_geometry_polar(rp, gp, bp)
     pix = scn.grid.pixels()
     d = 2 * np.linalg.norm(pix[:, None, :] - scn.tx[None, :, :], axis=2)
     assert info.k_lo <= math.floor(info.a1_bins_per_m * d.min())
     assert info.k_lo + info.n_bins - 1 >= math.floor(info.a1_bins_per_m * d.max()) + 1
-    assert info.updates_per_image == 70 * 40 * 40
-    # a tile spans 32 bearings x tile_y ranges: its half-diagonal bounds the window
-    rmax = scn.grid.r0 + (scn.grid.n_r - 1) * scn.grid.dr
-    rho_lo = 0.5 * math.hypot(31 * scn.grid.dth * scn.grid.r0, (info.tile_y - 1) * scn.grid.dr)
-    assert info.window_bins >= 4 * info.a1_bins_per_m * rho_lo
-    assert info.window_bins <= 4 * info.a1_bins_per_m * 0.5 * math.hypot(
-        32 * scn.grid.dth * rmax, info.tile_y * scn.grid.dr) * 1.01 + 8
+    assert info.updates_per_image == scn.grid.n_th * scn.grid.n_r * scn.n_chirps
+    # window: every pixel of every tile stays within the half window of the tile anchor's
+    # index, for every antenna position (brute force over tiles, chirps and pixels)
+    g, TX, TY = scn.grid, info.tile_x, info.tile_y
+    half = info.window_half_bins
+    assert info.window_bins >= 2 * half + 4
+    worst = 0.0
+    for j0 in range(0, g.n_r, TY):
+        for i0 in range(0, g.n_th, TX):
+            ra = g.r0 + (j0 + 0.5 * (TY - 1)) * g.dr
+            ta = g.th0 + (i0 + 0.5 * (TX - 1)) * g.dth
+            anc = np.array([g.xc + ra * np.sin(ta), g.yc + ra * np.cos(ta), g.zc])
+            pix = g.pixels(rows=np.arange(j0, min(j0 + TY, g.n_r)), cols=np.arange(i0, min(i0 + TX, g.n_th)))
+            dp = 2 * np.linalg.norm(pix[:, None, :] - scn.tx[None, :, :], axis=2)
+            da = 2 * np.linalg.norm(anc[None, :] - scn.tx, axis=1)
+            worst = max(worst, info.a1_bins_per_m * np.abs(dp - da[None, :]).max())
+    assert worst <= half
+    return info, worst
+
+
+def test_polar_window_is_tighter_than_the_triangle_bound(lib):
+    """Far polar tiles seen from near the polar centre: the window follows the range extent
+    of the tile, not its (much larger) half-diagonal."""
+    scn = sarsim.polar_small_config(n_chirps=40, ns=512, n_th=96, n_r=40, r0=20.0, dr=0.06, th0=-0.5, dth=0.01)
+    info, worst = _check_crop_and_window(scn)
+    TX, TY, g = info.tile_x, info.tile_y, scn.grid
+    rmax = g.r0 + ((g.n_r + TY - 1) // TY * TY) * g.dr
+    rho = 0.5 * math.hypot((TX - 1) * g.dth * rmax, (TY - 1) * g.dr)
+    assert info.window_bins < 0.5 * (4 * info.a1_bins_per_m * rho)
+    assert worst > 0.5 * info.window_half_bins       # and not needlessly wide
 
 
 def test_polar_plan_geometry_rejects_bad_grids(lib):
