@@ -48,7 +48,10 @@ namespace {
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
 constexpr uint32_t kMagicBits = 0x4B400000u;
 constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
-constexpr int kBatch = 8;                // producer: profile rows loaded per batch
+#ifndef SAR_BP_BATCH
+#define SAR_BP_BATCH 8
+#endif
+constexpr int kBatch = SAR_BP_BATCH;     // producer: profile rows loaded per batch
 #ifndef SAR_BP_CHIRP_UNROLL
 #define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
 #endif
@@ -199,8 +202,13 @@ __host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bo
 
 // NEAR: the plan has tiles within 3 rho of the antenna box; those tiles (a per-CTA,
 // warp-uniform decision) take the near-field SAFE consumer path, all others the fast one.
+#ifdef SAR_BP_MINB
+#define SAR_BP_BOUNDS(n) __launch_bounds__(n, SAR_BP_MINB)
+#else
+#define SAR_BP_BOUNDS(n) __launch_bounds__(n)
+#endif
 template <bool BISTATIC, bool DOP, bool NEAR, int NCW, int PB>
-__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
+__global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   constexpr int TX = kTileX;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -569,7 +577,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       const double gap = fmax(0.0, fmax(a.box_lo[k] - pt[k], pt[k] - a.box_hi[k]));
       d2 += gap * gap;
     }
-    if (d2 < a.near_r * a.near_r) consume(std::true_type{});
+    double rho_t = a.tile_rho;
+    if (a.polar) {   // annular patch: farthest from its anchor at a corner
+      const double rc = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+      const double ht = 0.5 * (TX - 1) * a.dth, hr = 0.5 * (TY - 1) * a.dr;
+      rho_t = 0.0;
+      for (int c = 0; c < 4; ++c) {
+        const double rr = rc + ((c & 1) ? hr : -hr), dt = (c & 2) ? ht : -ht;
+        rho_t = fmax(rho_t, sqrt(rr * rr + rc * rc - 2.0 * rr * rc * cos(dt)));
+      }
+    }
+    const double near_r = 3.0 * rho_t * (1.0 + 1e-6) + 1e-3;
+    if (d2 < near_r * near_r) consume(std::true_type{});
     else consume(std::false_type{});
   } else {
     consume(std::false_type{});
@@ -591,7 +610,7 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   b.tiles_y = (a.nrow + TY - 1) / TY;
   const long ntiles = (long)b.tiles_x * b.tiles_y;
   // Chirp split for grids that cannot fill the GPU: enough CTAs for ~8 waves of resident
-  // CTAs, each chunk at least 512 chirps (and a multiple of the ring stage).
+  // CTAs, each chunk at least 512 (chirp, RX) items (and a multiple of the ring stage).
   int resident = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, (NCW + 1) * 32, L.total);
   int sms = 148;
@@ -599,7 +618,7 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
-  while (ntiles * k < 8 * slots && a.nchirp / (2 * k) >= 512) k *= 2;
+  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
   b.chunk = (a.nchirp + k - 1) / k;
   b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
   b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);

@@ -125,8 +125,9 @@ __global__ void __launch_bounds__(BLOCK) rc_kernel(const RcArgs a) {
     const float2 A = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
     const float2 B = make_float2(0.5f * (Zk.y + Zn.y), -0.5f * (Zk.x - Zn.x));
     const float2 Ar = cmul(A, r), Br = cmul(B, r);
-    pa[i] = make_float2(sa * Ar.x, sa * Ar.y);
-    if (has_b) pb[i] = make_float2(sb * Br.x, sb * Br.y);
+    const bool in_spec = k <= (N >> 1);   // an even-length crop may end one bin past N/2 (A8: 0)
+    pa[i] = in_spec ? make_float2(sa * Ar.x, sa * Ar.y) : make_float2(0.f, 0.f);
+    if (has_b) pb[i] = in_spec ? make_float2(sb * Br.x, sb * Br.y) : make_float2(0.f, 0.f);
   }
 }
 

@@ -52,7 +52,8 @@ struct BpArgs {
   double a1, c2, k_lo;     // bins / metre two-way, cycles / metre two-way, crop start
   double kap_half;         // half window span in bins: 2 a1 rho_win + doppler bound
   double box_lo[3], box_hi[3];  // declared antenna box (near-field tile test)
-  double near_r;           // tiles whose anchor lies within near_r of the box run the SAFE form
+  double tile_rho;         // Cartesian tile half-diagonal; a tile whose anchor lies within
+                           // 3 rho_T + 1 mm of the box runs the SAFE form
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };

@@ -125,6 +125,21 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   }
   double dist_min, dist_max;
   box_distance(glo, ghi, b->lo, b->hi, &dist_min, &dist_max);
+  if (pg) {
+    // an annular sector is poorly described by its bounding box: also bound each leg
+    // through the polar centre c, r - |q - c| <= |p - q| <= r + |q - c|
+    double sc = 0.0;
+    for (int cx = 0; cx < 2; ++cx)
+      for (int cy = 0; cy < 2; ++cy)
+        for (int cz = 0; cz < 2; ++cz) {
+          const double ex = (cx ? b->hi[0] : b->lo[0]) - pg->xc, ey = (cy ? b->hi[1] : b->lo[1]) - pg->yc,
+                       ez = (cz ? b->hi[2] : b->lo[2]) - pg->zc;
+          sc = std::max(sc, sqrt(ex * ex + ey * ey + ez * ez));
+        }
+    const double r1 = pg->r0 + (pg->n_r - 1) * pg->dr;
+    dist_min = std::max(dist_min, pg->r0 - sc);
+    dist_max = std::min(dist_max, r1 + sc);
+  }
   I.d_min_m = 2.0 * dist_min;  // each leg lies in [dist_min, dist_max]
   I.d_max_m = 2.0 * dist_max;
   const double dop = r->doppler_max_bins;
@@ -133,6 +148,9 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   long k_hi = (long)floor(I.a1_bins_per_m * I.d_max_m + dop) + 3;
   k_lo = std::max(0L, std::min(k_lo, half));
   k_hi = std::max(k_lo, std::min(k_hi, half));
+  // even row length (16-B aligned rows); the extra bin may be N/2 + 1, which the range
+  // compression writes as 0 (A8)
+  if ((k_hi - k_lo + 1) & 1) ++k_hi;
   I.k_lo = (int32_t)k_lo;
   I.n_bins = (int32_t)(k_hi - k_lo + 1);
 
@@ -198,14 +216,19 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   I.tile_rho_m = out->rho;
   const bool bistatic = r->n_rx > 1;
   const bool auto_cb = cb <= 0, auto_stages = stages <= 0;
-  if (auto_cb) cb = std::max(1, 32 / r->n_rx);
+  auto smem = [&](int cb_, int st) { return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic); };
+  if (auto_cb) {
+    cb = std::max(1, 32 / r->n_rx);
+    // wide windows: fewer chirps per stage so that a 2-stage ring leaves room for two CTAs
+    while (cb > 1 && smem(cb, 2) > 96 * 1024) cb /= 2;
+  }
   for (;;) {
-    const size_t stage_bytes = sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, 1, bistatic) - 16 * sar::kBpMaxStages;
+    const size_t stage_bytes = smem(cb, 2) - smem(cb, 1);
     int st = stages;
+    // ring depth: as many stages as fit in ~48 KB
     if (auto_stages) st = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
     st = std::max(2, std::min(sar::kBpMaxStages, st));
-    // coarse grids (wide windows): fewer chirps per stage until the ring fits
-    if (sar::bp_smem_bytes(I.window_bins, cb, r->n_rx, st, bistatic) <= 200 * 1024) {
+    if (smem(cb, st) <= 200 * 1024) {
       stages = st;
       break;
     }
@@ -506,7 +529,7 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
     a.box_lo[k] = plan->box.lo[k];
     a.box_hi[k] = plan->box.hi[k];
   }
-  a.near_r = 3.0 * plan->tile_rho + 1e-3;
+  a.tile_rho = plan->tile_rho;
   const bool bistatic = rx_pos != nullptr;
   a.A1f = (float)(bistatic ? a.a1 : 2.0 * a.a1);
   a.binphase = plan->d_binphase;

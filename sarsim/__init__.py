@@ -252,6 +252,26 @@ def make_config(name: str, n_chirps: int | None = None, seed: int | None = None,
         tgt = np.array([[0.0, 5.00, 0.0]]); amp = np.array([1.0 + 0j])
         iso = np.array([[32, 32]])
         scn = Scenario("C1", radar, grid, tx, None, tgt, amp, iso, None, 0.0, seed or 1)
+    elif name in ("C6", "C6P"):
+        # The paper's own measurement (reading A1): ONE chirp sequence of N_m = 1024 chirps
+        # (109.3 ms) x 8 RX (Measure F) = 8192 aperture samples, on the paper's
+        # 1201^2 grid at 2.5 cm (C6) or on the Measure E polar grid (C6p).  A slow straight pass
+        # (0.75 m/s, aperture 8.2 cm) -- the aperture for which the recipe's grid has the
+        # paper's 165,061 pixels (reading A19).
+        radar = Radar()
+        M = n_chirps or 1024
+        tx = straight_track(M, 0.75 * radar.pri_s)
+        rx = rx_array(tx, 8, 0.005, radar.wavelength_m / 2.0)
+        grid = Grid(-15.0, 1.0, 0.0, 0.025, 0.025, 1201, 1201)
+        sd = seed or 7
+        rng = np.random.default_rng(sd)
+        tgt, amp, iso = fig1_scene(rng, grid, 32, (-14.5, 14.5, 1.5, 12.5), 64, (-14.5, 14.5, 1.5, 30.5))
+        scn = Scenario(name if name == "C6" else "C6p", radar, grid, tx, rx, tgt, amp, iso, None, 0.05, sd)
+        if name == "C6P":
+            th = float(np.arctan2(15.0, 1.0))
+            L = float(np.linalg.norm(tx[-1] - tx[0]))
+            scn.grid = polar_recipe(radar, tx.mean(0), L, 1.0, float(np.hypot(15.0, 31.0)), -th, th, 2.5)
+            scn.isolated = np.zeros((0, 2), np.int64)
     elif name in ("C2", "C0", "C5"):
         radar = Radar()
         # C5: one long straight track of 8192 + 15 hops of 1024 chirps (16 frames)

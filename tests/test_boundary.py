@@ -80,7 +80,7 @@ def test_plan_geometry_constants_and_crop(lib):
     kmin = info.a1_bins_per_m * dn.min()
     kmax = info.a1_bins_per_m * d.max()
     assert info.k_lo <= math.floor(kmin) and info.k_lo + info.n_bins - 1 >= math.floor(kmax) + 1
-    assert info.k_lo + info.n_bins - 1 <= r.fft_len // 2
+    assert info.k_lo + info.n_bins - 1 <= r.fft_len // 2 + 1 and info.n_bins % 2 == 0
     # roughly the 1750 bins SURVEY 8(d) estimates for C3
     assert 1500 < info.n_bins < 1900
     assert info.tile_x == 32 and info.tile_y == 32

@@ -381,7 +381,7 @@ def test_image_sum_kernel(cuda_lib):
 
 
 # ----------------------------------------------------------------------------- full-size configs
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4", "C6"])
 def test_full_size_config_sampled_parity(cuda_lib, cfg):
     """BASELINE configs at full size in the bench's launch configuration; the oracle on the
     C-6 sample (strided rows/cols + windows around isolated targets and GPU maxima)."""
@@ -390,7 +390,7 @@ def test_full_size_config_sampled_parity(cuda_lib, cfg):
     img, prof, plan = gpu_image(scn, raw, return_prof=True)
     a = np.abs(img.cpu().numpy())
     g = scn.grid
-    stride = {"C2": (97, 101), "C3": (149, 151), "C0": (61, 67), "C4": (397, 401)}[cfg]
+    stride = {"C2": (97, 101), "C3": (149, 151), "C0": (61, 67), "C4": (397, 401), "C6": (61, 67)}[cfg]
     idx = sample_indices(scn, a, stride=stride, win=2 if cfg == "C4" else 3)
     pix = g.pixel_list(idx)
     # oracle on the crop the plan keeps (it raises if any pixel needed a bin outside it)
@@ -399,12 +399,16 @@ def test_full_size_config_sampled_parity(cuda_lib, cfg):
     got = img.cpu().numpy()[idx[:, 0], idx[:, 1]]
     plan.close()
     assert rel_err(got, ref) <= REL_TOL
-    # global peak: the pole (a = 1) on both sides
-    pole = tuple(scn.isolated[0])
-    assert np.unravel_index(np.argmax(a), a.shape) == pole
+    # global peak: the oracle's maximum over the sample (which holds windows around the GPU's
+    # maxima) sits at the GPU's global argmax; with the 7 m apertures that is the pole (a = 1)
     k = np.argmax(np.abs(ref))
-    assert tuple(idx[k]) == pole
-    # local argmax of every isolated target agrees (within its sampled window)
+    assert tuple(idx[k]) == np.unravel_index(np.argmax(a), a.shape)
+    if cfg != "C6":    # C6's 8 cm aperture resolves ~0.2 m in azimuth: the wall outshines the pole
+        assert tuple(idx[k]) == tuple(scn.isolated[0])
+    # local argmax of every isolated target agrees (within its sampled window) wherever the
+    # oracle's peak is unambiguous (best/second > 1 + 4e-3, reading A15)
     for (j, i) in scn.isolated:
         sel = (np.abs(idx[:, 0] - j) <= 2) & (np.abs(idx[:, 1] - i) <= 2)
-        assert np.argmax(np.abs(got[sel])) == np.argmax(np.abs(ref[sel]))
+        r = np.sort(np.abs(ref[sel]))
+        if r[-1] > (1 + 4e-3) * r[-2]:
+            assert np.argmax(np.abs(got[sel])) == np.argmax(np.abs(ref[sel]))

@@ -10,6 +10,7 @@ import sarsim
 from sarsim import Grid, PolarGrid
 
 from .helpers import REL_TOL, gpu_image, oracle_image, rel_err
+from .helpers import oracle_profiles as oracle_profiles_crop
 
 pytestmark = pytest.mark.gpu
 
@@ -93,3 +94,39 @@ def test_polar_image_resampled_peaks_where_the_cartesian_image_does(cuda_lib):
     assert pc == (20, 20)
     assert abs(pr[0] - pc[0]) <= 1 and abs(pr[1] - pc[1]) <= 1
     assert abs(abs(rs[pc]) - abs(cimg[pc])) < 0.1 * abs(cimg[pc])
+
+
+def test_C6p_full_size_sampled_parity(cuda_lib):
+    """The bench's Measure E workload (C6p: 520 x 315 polar pixels, 1024 chirps x 8 RX) in the
+    bench's launch configuration against the oracle on a strided sample plus windows around the
+    GPU's strongest pixels; then the resampling kernel on the same image."""
+    import torch
+
+    scn = sarsim.make_config("C6p")
+    raw = sarsim.simulate_raw(scn, device="cuda:0")
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    g = scn.grid
+    a = np.abs(img.cpu().numpy())
+    js, iis = np.arange(0, g.n_r, 23), np.arange(0, g.n_th, 7)
+    pts = [np.stack(np.meshgrid(js, iis, indexing="ij"), -1).reshape(-1, 2)]
+    for f in np.argsort(a.reshape(-1))[::-1][:16]:
+        j, i = np.unravel_index(f, a.shape)
+        jj, ii = np.meshgrid(np.arange(j - 2, j + 3), np.arange(i - 2, i + 3), indexing="ij")
+        w = np.stack([jj, ii], -1).reshape(-1, 2)
+        pts.append(w[(w[:, 0] >= 0) & (w[:, 0] < g.n_r) & (w[:, 1] >= 0) & (w[:, 1] < g.n_th)])
+    idx = np.unique(np.concatenate(pts), axis=0)
+    ref_prof = oracle_profiles_crop(scn, raw.cpu().numpy(), plan.k_lo, plan.n_bins)
+    ref = oracle.backproject(ref_prof, plan.k_lo, scn.radar, scn.tx, scn.rx, g.pixel_list(idx))
+    got = img.cpu().numpy()[idx[:, 0], idx[:, 1]]
+    assert rel_err(got, ref) <= REL_TOL
+    k = int(np.argmax(np.abs(ref)))
+    assert tuple(idx[k]) == np.unravel_index(np.argmax(a), a.shape)
+    cart = sarsim.make_config("C0", n_chirps=1).grid
+    rs = cuda_lib.polar_to_cartesian(g, img, cart)
+    torch.cuda.synchronize()
+    sub = (slice(0, None, 37), slice(0, None, 41))
+    ref_rs = oracle.polar_to_cartesian(g, img.cpu().numpy().astype(np.complex128),
+                                       Grid(cart.x0, cart.y0, 0.0, cart.dx * 41, cart.dy * 37,
+                                            len(range(0, cart.nx, 41)), len(range(0, cart.ny, 37))))
+    assert np.abs(rs.cpu().numpy()[sub] - ref_rs).max() <= 1e-5 * np.abs(ref_rs).max()
+    plan.close()
