@@ -202,13 +202,8 @@ __host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bo
 
 // NEAR: the plan has tiles within 3 rho of the antenna box; those tiles (a per-CTA,
 // warp-uniform decision) take the near-field SAFE consumer path, all others the fast one.
-#ifdef SAR_BP_MINB
-#define SAR_BP_BOUNDS(n) __launch_bounds__(n, SAR_BP_MINB)
-#else
-#define SAR_BP_BOUNDS(n) __launch_bounds__(n)
-#endif
 template <bool BISTATIC, bool DOP, bool NEAR, int NCW, int PB>
-__global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
+__device__ __forceinline__ void bp_body(const BpArgs& a) {
   constexpr int TX = kTileX;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -274,7 +269,7 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
           const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
-          srec[2 * c + 1] = make_float4(NEAR ? (float)(Dz * Dz) : 0.f, 0.f, 0.f, 0.f);
+          srec[2 * c + 1] = make_float4(0.f, 0.f, NEAR ? (float)(Dz * Dz) : 0.f, 0.f);
         }
       }
       for (int e = lane; e < items; e += 32) {
@@ -312,8 +307,8 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
         const uint32_t off = waddr + 16u * (uint32_t)wh - 16u * kMagicBits;
         const int ri = BISTATIC ? a.CB + e : e;
         srec[2 * ri] = leg0;
-        srec[2 * ri + 1] = make_float4(NEAR ? (float)(dz * dz) : 0.f,
-                                       (float)(kap - k0 - 0.5 - wh), 0.f, __uint_as_float(off));
+        srec[2 * ri + 1] = make_float4((float)(kap - k0 - 0.5 - wh), __uint_as_float(off),
+                                       NEAR ? (float)(dz * dz) : 0.f, 0.f);
         skw[e] = make_int2(k0, (m * a.n_rx + n) * a.n_bins);
       }
       __syncwarp();
@@ -419,7 +414,9 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   int slot = 0;
   uint32_t parity = 0;
   for (int it = 0; it < n_iter; ++it) {
+#ifndef SAR_BP_NOWAIT
     mbar_wait(bar_full + 8 * slot, parity);
+#endif
     const int cnt = min(a.CB, nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
     if (kPaired) {
@@ -450,9 +447,10 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
       if (!BISTATIC) {
 #pragma unroll kChirpUnroll
         for (int c = 0; c < cnt; ++c) {
-          const float4 A = srec[2 * c], B = srec[2 * c + 1];
+          const float4 A = srec[2 * c];
+          const float2 B = *reinterpret_cast<const float2*>(srec + 2 * c + 1);
 #pragma unroll
-          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.y, __float_as_uint(B.w));
+          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.x, __float_as_uint(B.y));
         }
       } else {
 #pragma unroll 1
@@ -461,13 +459,14 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
           f32x2 DT[PB / 2];
 #pragma unroll
           for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
+          const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
 #pragma unroll 1
-          for (int n = 0; n < a.n_rx; ++n) {
-            const int ri = a.CB + c * a.n_rx + n;
-            const float4 A = srec[2 * ri], B = srec[2 * ri + 1];
+          for (int n = 0; n < a.n_rx; ++n, rp += 2) {
+            const float4 A = rp[0];
+            const float2 B = *reinterpret_cast<const float2*>(rp + 1);
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h)
-              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.y, __float_as_uint(B.w));
+              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.x, __float_as_uint(B.y));
           }
         }
       }
@@ -475,11 +474,11 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
 #pragma unroll kChirpUnroll
       for (int c = 0; c < cnt; ++c) {
         const float4 A = srec[2 * c], B = srec[2 * c + 1];
-        const uint32_t off = __float_as_uint(B.w);
+        const uint32_t off = __float_as_uint(B.y);
 #pragma unroll
         for (int p = 0; p < PB; ++p) {
-          const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
-          float kap = fmaf(A1, dR, B.y);
+          const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+          float kap = fmaf(A1, dR, B.x);
           if (DOP) kap += fd[p];
           const float tk = kap + kMagic;
           const float kf = tk - kMagic;
@@ -500,16 +499,16 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
         const float4 T = srec[2 * c], TB = srec[2 * c + 1];
         float dT[PB];
 #pragma unroll
-        for (int p = 0; p < PB; ++p) dT[p] = leg_delta<SAFE>(T.x, T.y, T.z, T.w, TB.x, ux[p], uy[p], wh[p]);
+        for (int p = 0; p < PB; ++p) dT[p] = leg_delta<SAFE>(T.x, T.y, T.z, T.w, TB.z, ux[p], uy[p], wh[p]);
 #pragma unroll 1
         for (int n = 0; n < a.n_rx; ++n) {
           const int ri = a.CB + c * a.n_rx + n;
           const float4 A = srec[2 * ri], B = srec[2 * ri + 1];
-          const uint32_t off = __float_as_uint(B.w);
+          const uint32_t off = __float_as_uint(B.y);
 #pragma unroll
           for (int p = 0; p < PB; ++p) {
-            const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
-            float kap = fmaf(A1, dR, B.y);
+            const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+            float kap = fmaf(A1, dR, B.x);
             if (DOP) kap += fd[p];
             const float tk = kap + kMagic;
             const float kf = tk - kMagic;
@@ -595,9 +594,30 @@ __global__ void SAR_BP_BOUNDS((NCW + 1) * 32) bp_kernel(const BpArgs a) {
   }
 }
 
+// Register budget: the monostatic kernel is left to ptxas (a min-blocks bound changes its
+// schedule and was measured 5 % slower on C3); the bistatic kernel (TX leg kept live across
+// the RX loop) is held to four resident CTAs per SM at the default 32 x 32 tile:
+// C4 1343 -> 1190 ms (tools/vsweep.sh).
+template <bool DOP, bool NEAR, int NCW, int PB>
+__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel_mono(const BpArgs a) {
+  bp_body<false, DOP, NEAR, NCW, PB>(a);
+}
+template <bool DOP, bool NEAR, int NCW, int PB>
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? 4 : 1) bp_kernel_bi(const BpArgs a) {
+  bp_body<true, DOP, NEAR, NCW, PB>(a);
+}
+template <bool BI, bool DOP, bool NEAR, int NCW, int PB>
+struct BpKernel {
+  static constexpr auto fn = bp_kernel_mono<DOP, NEAR, NCW, PB>;
+};
+template <bool DOP, bool NEAR, int NCW, int PB>
+struct BpKernel<true, DOP, NEAR, NCW, PB> {
+  static constexpr auto fn = bp_kernel_bi<DOP, NEAR, NCW, PB>;
+};
+
 template <bool BI, bool DOP, bool SAFE, int NCW, int PB>
 cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
-  auto kern = bp_kernel<BI, DOP, SAFE, NCW, PB>;
+  auto kern = BpKernel<BI, DOP, SAFE, NCW, PB>::fn;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
   static int configured_bytes = -1;
