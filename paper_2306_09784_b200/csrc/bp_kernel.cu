@@ -59,6 +59,33 @@ constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
 // (A min-blocks launch bound, even "1", changes ptxas's schedule: measured 5 % slower on C3;
 //  capping registers for 6-7 resident CTAs spilled and was slower too.  tools/vsweep.sh)
 
+#ifdef SAR_BP_TRACE
+// tuning instrumentation (tools/trace_bp.py): clock64 stamps of the ring waits of four CTAs
+constexpr int kTrCtas = 4, kTrIt = 256;
+__device__ unsigned long long g_trace[kTrCtas][9][kTrIt][3];
+__device__ unsigned int g_trace_wid[kTrCtas][9][2];
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int tr_cta() {
+  const int b = blockIdx.x;
+  return b == 2000 ? 0 : b == 2001 ? 1 : b == 5000 ? 2 : b == 5001 ? 3 : -1;
+}
+__device__ __forceinline__ void tr_ids(int trc, int w) {
+  unsigned int wid, smid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  g_trace_wid[trc][w][0] = wid;
+  g_trace_wid[trc][w][1] = smid;
+}
+#define SAR_TR(w, it, k) \
+  if (trc >= 0 && lane == 0 && (it) < kTrIt) g_trace[trc][w][it][k] = clk()
+#else
+#define SAR_TR(w, it, k)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -254,8 +281,14 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     float4* win = reinterpret_cast<float4*>(smem + L.win);
     int slot = 0;
     uint32_t parity = 0;
+#ifdef SAR_BP_TRACE
+    const int trc = tr_cta();
+    if (trc >= 0 && lane == 0) tr_ids(trc, 8);
+#endif
     for (int it = 0; it < n_iter; ++it) {
+      SAR_TR(8, it, 0);
       mbar_wait(bar_empty + 8 * slot, parity ^ 1);
+      SAR_TR(8, it, 1);
       const int c0 = it * a.CB;
       const int cnt = min(a.CB, nchirp - c0);
       const int items = cnt * a.n_rx;
@@ -348,6 +381,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         }
       }
       mbar_arrive(bar_full + 8 * slot);
+      SAR_TR(8, it, 2);
       if (++slot == S) {
         slot = 0;
         parity ^= 1;
@@ -413,10 +447,14 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 
   int slot = 0;
   uint32_t parity = 0;
-  for (int it = 0; it < n_iter; ++it) {
-#ifndef SAR_BP_NOWAIT
-    mbar_wait(bar_full + 8 * slot, parity);
+#ifdef SAR_BP_TRACE
+  const int trc = tr_cta();
+  if (trc >= 0 && lane == 0) tr_ids(trc, warp);
 #endif
+  for (int it = 0; it < n_iter; ++it) {
+    SAR_TR(warp, it, 0);
+    mbar_wait(bar_full + 8 * slot, parity);
+    SAR_TR(warp, it, 1);
     const int cnt = min(a.CB, nchirp - it * a.CB);
     const float4* srec = rec + (size_t)slot * L.legs * 2;
     if (kPaired) {
@@ -524,6 +562,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
       }
     }
     mbar_arrive(bar_empty + 8 * slot);
+    SAR_TR(warp, it, 2);
     if (++slot == S) {
       slot = 0;
       parity ^= 1;
@@ -680,3 +719,10 @@ cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, c
 }
 
 }  // namespace sar
+
+#ifdef SAR_BP_TRACE
+extern "C" int sar_debug_trace(void* dst, void* dst_wid) {
+  cudaMemcpyFromSymbol(dst, sar::g_trace, sizeof(sar::g_trace));
+  return (int)cudaMemcpyFromSymbol(dst_wid, sar::g_trace_wid, sizeof(sar::g_trace_wid));
+}
+#endif
