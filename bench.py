@@ -239,6 +239,16 @@ def run_ours(args):
     prof = plan.empty_profiles()
     local_img = plan.empty_image(nrow)
     full_img = torch.empty((g.ny, g.nx), dtype=torch.complex64, device=dev) if world > 1 else local_img
+    # N > 1: the image gather fused into the BP epilogue (NEXT-4, symmetric memory: P2P stores
+    # or one multimem.st per tile); --gather nccl keeps the separate all_gather
+    fused, fused_err = None, None
+    if world > 1 and args.gather in ("fused", "multicast"):
+        from paper_2306_09784_b200.dist import FusedRowGather
+
+        try:
+            fused = FusedRowGather(g.ny, g.nx, dev, prefer_multicast=args.gather == "multicast")
+        except Exception as e:  # no symmetric memory on this system: report and use NCCL
+            fused_err = repr(e)[:200]
     polar = plan.polar
     if polar:   # Measure E: the polar image is resampled onto the Cartesian C0 grid in the step
         import sarsim
@@ -251,9 +261,15 @@ def run_ours(args):
     def step():
         plan.range_compress(raw, wsar, out=prof, stream=stream)
         ev[1].record(stream)
-        plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
-        ev[2].record(stream)
-        if world > 1:
+        if fused is not None:
+            plan.backproject_scatter(prof, tx, fused.ptrs, rx, row0=row0, nrow=nrow, multicast=fused.multicast,
+                                     stream=stream)
+            ev[2].record(stream)
+            fused.barrier()
+        else:
+            plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
+            ev[2].record(stream)
+        if world > 1 and fused is None:
             dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1),
                                         torch.view_as_real(local_img).view(-1))
         if polar:
@@ -286,6 +302,17 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     launches = plan.launches - l0
+    gather_check = None
+    if fused is not None:
+        # outside the timed region: the fused image must equal the NCCL gather of the rows
+        plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
+        from paper_2306_09784_b200.dist import gather_rows
+
+        ref = gather_rows(local_img, g.ny)
+        torch.cuda.synchronize()
+        gather_check = bool(torch.equal(ref, fused.image))
+        if not gather_check:
+            print("bench: fused gather differs from the NCCL gather", file=sys.stderr)
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms, sum(bp_ms)], dtype=torch.float64, device=dev)
@@ -359,10 +386,15 @@ def run_ours(args):
             "config": {"workload": WORKLOADS[args.config], "config": args.config, "pixels": g.nx * g.ny,
                        "chirps": scn.n_chirps, "n_rx": scn.n_rx, "samples": scn.radar.n_samples,
                        "fft_len": scn.radar.fft_len, "n_bins": plan.n_bins, "updates": scn.updates,
-                       "parallelism": f"pixel rows x{world}" + (" + NCCL all_gather" if world > 1 else ""),
+                       "parallelism": f"pixel rows x{world}" + (
+                           "" if world == 1 else
+                           (f" + gather fused into the BP epilogue ({'multimem.st' if fused.multicast else 'P2P stores'},"
+                            f" symmetric memory)" if fused is not None else " + NCCL all_gather")),
+                       "gather_check": gather_check, "fused_gather_error": fused_err,
                        "l2": "256 MB buffer written between timed steps (outside the event span)",
-                       "step": "sar_range_compress(all chirps) + sar_backproject(rank rows)"
-                               + (" + all_gather_into_tensor" if world > 1 else "")
+                       "step": "sar_range_compress(all chirps) + "
+                               + ("sar_backproject_scatter(rank rows -> every rank's image) + barrier" if fused is not None
+                                  else "sar_backproject(rank rows)" + (" + all_gather_into_tensor" if world > 1 else ""))
                                + (" + sar_polar_to_cartesian" if polar else "")},
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -499,6 +531,9 @@ def main(argv=None):
     ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", default="fused", choices=["fused", "multicast", "nccl"],
+                    help="N > 1: image gather fused into the BP epilogue (symmetric memory; P2P stores, or "
+                         "multimem.st to the NVSwitch multicast address) or a separate NCCL all_gather")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -182,6 +182,22 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
                              int32_t row0, int32_t nrow, sar_complex64_t* image,
                              int32_t accumulate, sar_stream_t stream);
 
+/* Back-projection with the image gather fused into the epilogue (NEXT-4; north star's
+ * multi-GPU design): the same computation as sar_backproject for rows
+ * [row0, row0 + nrow), but every finished tile is stored (not accumulated) at its ABSOLUTE
+ * rows row0 + j of each full image images[d] (complex [ny][nx], d < n_images <= 8), while the
+ * remaining tiles are still being computed.  With symmetric memory the images are the
+ * P2P-mapped buffers of every rank (one NVLink store per peer), or, with multicast = 1,
+ * one multicast address (n_images = 1) that the NVSwitch delivers to every rank
+ * (multimem.st).  Rows outside [row0, row0 + nrow) are not touched; the caller orders
+ * the ranks (e.g. a symmetric-memory barrier) before reading.  No chirp split.
+ *   images  host array of n_images device pointers (may be peer or multicast addresses) */
+sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* profiles,
+                                     const double* tx_pos, const double* rx_pos,
+                                     const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                                     int32_t row0, int32_t nrow, sar_complex64_t* const* images,
+                                     int32_t n_images, int32_t multicast, sar_stream_t stream);
+
 /* End-to-end image formation from HOST buffers (the paper's "Load" + "BP",
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a
  * plan-owned device workspace, runs sar_range_compress over all chirps and

@@ -589,7 +589,18 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     }
     if (gx[p] < a.nx && gy[p] < a.nrow) {
       float2* dst = a.img + (size_t)gy[p] * a.nx + gx[p];
-      if (a.ksplit > 1) {
+      if (a.n_peer > 0) {
+        // fused gather (NEXT-4): the finished tile goes straight to every rank's full image
+        // over NVLink while other tiles are still being computed
+        const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
+        if (a.multicast) {
+          asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(a.peer[0] + o),
+                       "f"(acc_r[p]), "f"(acc_i[p])
+                       : "memory");
+        } else {
+          for (int d = 0; d < a.n_peer; ++d) a.peer[d][o] = make_float2(acc_r[p], acc_i[p]);
+        }
+      } else if (a.ksplit > 1) {
         // several chirp chunks add into the same pixel (the image was zeroed first when
         // not accumulating); fire-and-forget reductions in L2
         float* d = reinterpret_cast<float*>(dst);
@@ -675,7 +686,7 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
-  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
+  while (a.n_peer == 0 && ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
   b.chunk = (a.nchirp + k - 1) / k;
   b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
   b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);

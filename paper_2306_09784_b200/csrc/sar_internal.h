@@ -54,6 +54,11 @@ struct BpArgs {
   double box_lo[3], box_hi[3];  // declared antenna box (near-field tile test)
   double tile_rho;         // Cartesian tile half-diagonal; a tile whose anchor lies within
                            // 3 rho_T + 1 mm of the box runs the SAFE form
+  // NEXT-4 scatter epilogue: when n_peer > 0 the tile is stored at absolute rows row0 + j of
+  // every full image peer[d] ([ny][nx]; P2P-mapped peer buffers, or one multicast address
+  // written with multimem.st when multicast != 0) instead of img
+  float2* peer[8];
+  int n_peer, multicast;
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };

@@ -470,11 +470,12 @@ sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* 
   return SAR_OK;
 }
 
-sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
-                             const double* tx_pos, const double* rx_pos,
-                             const float* doppler_bins, int32_t chirp0, int32_t nchirp,
-                             int32_t row0, int32_t nrow, sar_complex64_t* image,
-                             int32_t accumulate, sar_stream_t stream) {
+namespace {
+sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, const double* tx_pos,
+                              const double* rx_pos, const float* doppler_bins, int32_t chirp0,
+                              int32_t nchirp, int32_t row0, int32_t nrow, sar_complex64_t* image,
+                              int32_t accumulate, sar_complex64_t* const* peers, int32_t n_peer,
+                              int32_t multicast, sar_stream_t stream) {
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   const sar_radar_params_t& r = plan->radar;
   const sar_grid_t& g = plan->grid;
@@ -534,11 +535,40 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
   a.A1f = (float)(bistatic ? a.a1 : 2.0 * a.a1);
   a.binphase = plan->d_binphase;
   a.C3f = (float)(2.0 * sar::kPi * a.c2 / a.a1);
+  a.n_peer = n_peer;
+  a.multicast = multicast;
+  for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
   plan->launches.fetch_add(1);
   return SAR_OK;
+}
+}  // namespace
+
+sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
+                             const double* tx_pos, const double* rx_pos,
+                             const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                             int32_t row0, int32_t nrow, sar_complex64_t* image,
+                             int32_t accumulate, sar_stream_t stream) {
+  return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, row0, nrow, image,
+                          accumulate, nullptr, 0, 0, stream);
+}
+
+sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* profiles,
+                                     const double* tx_pos, const double* rx_pos,
+                                     const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                                     int32_t row0, int32_t nrow, sar_complex64_t* const* images,
+                                     int32_t n_images, int32_t multicast, sar_stream_t stream) {
+  if (!images || n_images < 1 || n_images > 8)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "images must hold 1..8 device pointers");
+  if (multicast != 0 && multicast != 1) return fail(SAR_ERR_INVALID_ARGUMENT, "multicast must be 0 or 1");
+  if (multicast && n_images != 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "a multicast store takes exactly one (multicast) address");
+  for (int d = 0; d < n_images; ++d)
+    if (!images[d]) return fail(SAR_ERR_INVALID_ARGUMENT, "null image pointer");
+  return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, row0, nrow, images[0],
+                          0, images, n_images, multicast, stream);
 }
 
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,

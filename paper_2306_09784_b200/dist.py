@@ -7,8 +7,12 @@ Two decompositions of the same sum P(p) = sum_m sum_n (...)  (Alg. 2 L12, P:L476
   * chirps      -- rank r owns chirps [c0, c0 + nc); it range-compresses only those and
     back-projects ALL pixels into a partial image; one reduce(SUM) to the root adds the
     partial images (complex addition is component-wise on the float32 view).
-The compute calls go through libsar (``sar.Plan``); the helpers below only partition
-and move bytes, so they also run with the gloo backend on CPU tensors in the tests.
+  * pixel rows, gather fused (NEXT-4) -- ``FusedRowGather``: every rank's full image lives in
+    symmetric memory; the BP epilogue stores each finished tile into all ranks' images over
+    NVLink (P2P stores, or one multimem.st to the NVSwitch multicast address), so the gather
+    overlaps the compute and no collective runs afterwards (one symmetric-memory barrier).
+The compute calls go through libsar (``sar.Plan``); the other helpers only partition and
+move bytes, so they also run with the gloo backend on CPU tensors in the tests.
 """
 from __future__ import annotations
 
@@ -65,3 +69,31 @@ def reduce_partials(partial, dst: int = 0, group=None):
 
     dist.reduce(torch.view_as_real(partial).reshape(-1), dst=dst, op=dist.ReduceOp.SUM, group=group)
     return partial
+
+
+class FusedRowGather:
+    """Full [ny][nx] complex64 image in symmetric memory on every rank (torch
+    ``_symmetric_memory``) + the device addresses the BP scatter epilogue writes to.
+
+    ``ptrs`` are the P2P-mapped buffers of all ranks (``multicast=False``) or the single
+    multicast address (``multicast=True``, when the NVSwitch supports it and
+    ``prefer_multicast``).  After the scatter launch, ``barrier()`` orders every rank's
+    stores before any rank reads ``image``."""
+
+    def __init__(self, ny: int, nx: int, device, group=None, prefer_multicast: bool = True):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        group = group or dist.group.WORLD
+        self.world = dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("the scatter epilogue addresses at most 8 ranks")
+        self.buf = symm_mem.empty((ny, 2 * nx), dtype=torch.float32, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, group.group_name)
+        self.image = torch.view_as_complex(self.buf.view(ny, nx, 2))
+        self.multicast = bool(prefer_multicast and self.hdl.multicast_ptr)   # 0 without NVLS multicast
+        self.ptrs = [int(self.hdl.multicast_ptr)] if self.multicast else [int(p) for p in self.hdl.buffer_ptrs]
+
+    def barrier(self, channel: int = 0):
+        self.hdl.barrier(channel=channel)

@@ -80,6 +80,9 @@ def load() -> ctypes.CDLL:
             lib.sar_plan_crop.argtypes = [_vp, P(_i32), P(_i32)]
             lib.sar_range_compress.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_backproject.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp]
+            lib.sar_backproject_scatter.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, P(_vp), _i32,
+                                                    _i32, _vp]
+            lib.sar_backproject_scatter.restype = ctypes.c_int
             lib.sar_form_image.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
                                               P(ctypes.c_double * 3), _vp, _vp]
@@ -176,6 +179,13 @@ def sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row
                     accumulate=0, stream=0):
     _check(load().sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow,
                                   img_ptr, accumulate, stream))
+
+
+def sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow, image_ptrs,
+                            multicast=0, stream=0):
+    arr = (_vp * len(image_ptrs))(*image_ptrs)
+    _check(load().sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow,
+                                          arr, len(image_ptrs), int(multicast), stream))
 
 
 def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream=0):
@@ -362,6 +372,23 @@ class Plan:
                         _dptr(out, torch.complex64, (nrow, self.grid.nx), "image"), int(bool(accumulate)),
                         _stream_handle(stream))
         return out
+
+    def backproject_scatter(self, profiles, tx, image_ptrs, rx=None, doppler=None, chirp0=0, nchirp=None, row0=0,
+                            nrow=None, multicast=False, stream=None):
+        """Back-project rows [row0, row0+nrow) and store each finished tile at its absolute rows of
+        every full image in ``image_ptrs`` (device addresses: local, P2P-mapped peer buffers, or
+        one multicast address with ``multicast=True``) -- the gather fused into the epilogue."""
+        import torch
+
+        nchirp = self.n_chirps - chirp0 if nchirp is None else nchirp
+        nrow = self.grid.ny - row0 if nrow is None else nrow
+        sar_backproject_scatter(self.handle,
+                                _dptr(profiles, torch.complex64, (self.n_chirps, self.n_rx, self.n_bins), "profiles"),
+                                _dptr(tx, torch.float64, (self.n_chirps, 3), "tx"),
+                                _dptr(rx, torch.float64, (self.n_chirps, self.n_rx, 3), "rx"),
+                                _dptr(doppler, torch.float32, (self.grid.ny, self.grid.nx), "doppler"),
+                                chirp0, nchirp, row0, nrow, [int(p) for p in image_ptrs], int(bool(multicast)),
+                                _stream_handle(stream))
 
     def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, row0=0, nrow=None, out_h=None,
                    stream=None, sync=True):

@@ -1,0 +1,84 @@
+"""NEXT-4 fused gather on one GPU: the BP scatter epilogue (sar_backproject_scatter) writes the
+rank's rows into several full images at once -- here local buffers standing in for P2P-mapped
+peers (no cross-rank waiting is involved), and, where the NVSwitch supports it, a one-rank
+symmetric-memory multicast address (multimem.st).  Rows outside the shard stay untouched and
+the stored rows equal sar_backproject's bit for bit."""
+import numpy as np
+import pytest
+
+import sarsim
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cuda_lib):
+    import torch
+
+    scn = sarsim.small_config(n_chirps=64, ns=256, nx=77, ny=70, seed=51)
+    raw = sarsim.simulate_raw(scn, device="cuda:0")
+    lo, hi = scn.antenna_box(1e-3)
+    plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, 1, (lo, hi))
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    prof = plan.range_compress(raw)
+    return scn, plan, tx, prof
+
+
+@pytest.mark.parametrize("rows", [(0, 70), (32, 32), (13, 40)])
+def test_scatter_to_several_images_equals_backproject(cuda_lib, rows):
+    import torch
+
+    scn, plan, tx, prof = _setup(cuda_lib)
+    row0, nrow = rows
+    g = scn.grid
+    ref = plan.backproject(prof, tx, row0=row0, nrow=nrow)
+    imgs = [torch.full((g.ny, g.nx), complex(7.0, -7.0), dtype=torch.complex64, device="cuda:0") for _ in range(3)]
+    plan.backproject_scatter(prof, tx, [im.data_ptr() for im in imgs], row0=row0, nrow=nrow)
+    torch.cuda.synchronize()
+    for im in imgs:
+        assert torch.equal(im[row0:row0 + nrow], ref)
+        assert torch.all(im[:row0] == complex(7.0, -7.0)) and torch.all(im[row0 + nrow:] == complex(7.0, -7.0))
+    plan.close()
+
+
+def test_scatter_argument_errors(cuda_lib):
+    from paper_2306_09784_b200 import sar
+
+    scn, plan, tx, prof = _setup(cuda_lib)
+    with pytest.raises(sar.SarError):
+        plan.backproject_scatter(prof, tx, [])
+    with pytest.raises(sar.SarError):
+        plan.backproject_scatter(prof, tx, [prof.data_ptr()] * 9)
+    with pytest.raises(sar.SarError):
+        plan.backproject_scatter(prof, tx, [prof.data_ptr(), prof.data_ptr()], multicast=True)
+    plan.close()
+
+
+def test_symmetric_memory_one_rank(cuda_lib):
+    """The bench's N > 1 path on a one-rank group: symmetric-memory image, scatter epilogue
+    through the multicast address when available (else the rank's own mapped buffer)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_09784_b200.dist import FusedRowGather
+
+    scn, plan, tx, prof = _setup(cuda_lib)
+    g = scn.grid
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda:0"))
+    try:
+        fg = FusedRowGather(g.ny, g.nx, torch.device("cuda:0"))
+        fg.image.fill_(complex(3.0, 3.0))
+        torch.cuda.synchronize()
+        plan.backproject_scatter(prof, tx, fg.ptrs, multicast=fg.multicast)
+        fg.barrier()
+        torch.cuda.synchronize()
+        ref = plan.backproject(prof, tx)
+        torch.cuda.synchronize()
+        assert torch.equal(fg.image, ref), f"multicast={fg.multicast}"
+        print("multicast path:", fg.multicast)
+    finally:
+        plan.close()
+        if own:
+            dist.destroy_process_group()
