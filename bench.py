@@ -443,6 +443,16 @@ def run_stream(args):
     img = torch.empty((g0.ny, g0.nx), dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
     c_lo, c_n = chirp_partition(8192, world, rank)
+    # N > 1: the chirp-shard reduction fused into the BP epilogue (P2P red.add into rank 0's
+    # symmetric-memory image; --gather nccl keeps the separate reduce)
+    fused = None
+    if world > 1 and args.gather in ("fused", "multicast") and args.config != "C5i":
+        from paper_2306_09784_b200.dist import FusedRowGather
+
+        try:
+            fused = FusedRowGather(g0.ny, g0.nx, dev, prefer_multicast=False)
+        except Exception as e:
+            print(f"bench: fused reduce unavailable ({e!r}); using NCCL", file=sys.stderr)
 
     incremental = args.config == "C5i"
     if incremental:
@@ -469,6 +479,14 @@ def run_stream(args):
         plan = plans[f % len(frames)]
         prof = prof_buf[: scn.n_chirps * plan.n_bins].view(scn.n_chirps, 1, plan.n_bins)
         plan.range_compress(raw, wsar, chirp0=c0 + c_lo, nchirp=c_n, out=prof, stream=stream)
+        if fused is not None:
+            if rank == 0:
+                fused.image.zero_()
+            fused.barrier()
+            plan.backproject_scatter(prof, tx, fused.root_ptrs(0), chirp0=c0 + c_lo, nchirp=c_n, add=True,
+                                     stream=stream)
+            fused.barrier()
+            return
         plan.backproject(prof, tx, chirp0=c0 + c_lo, nchirp=c_n, out=img, stream=stream)
         if world > 1:
             reduce_partials(img, dst=0)
@@ -510,7 +528,10 @@ def run_stream(args):
             "realtime_budget_ms": 1024 * scn.radar.pri_s * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload, "config": args.config,
-                       "parallelism": f"chirps x{world}" + (" + NCCL reduce" if world > 1 else ""),
+                       "parallelism": f"chirps x{world}" + (
+                           "" if world == 1 else
+                           " + reduction fused into the BP epilogue (P2P red.add, symmetric memory)" if fused is not None
+                           else " + NCCL reduce"),
                        "step": step},
             "gpu_launches": launches, "clocks": clk.summary(),
         }), flush=True)

@@ -182,21 +182,27 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
                              int32_t row0, int32_t nrow, sar_complex64_t* image,
                              int32_t accumulate, sar_stream_t stream);
 
-/* Back-projection with the image gather fused into the epilogue (NEXT-4; north star's
- * multi-GPU design): the same computation as sar_backproject for rows
- * [row0, row0 + nrow), but every finished tile is stored (not accumulated) at its ABSOLUTE
- * rows row0 + j of each full image images[d] (complex [ny][nx], d < n_images <= 8), while the
- * remaining tiles are still being computed.  With symmetric memory the images are the
- * P2P-mapped buffers of every rank (one NVLink store per peer), or, with multicast = 1,
- * one multicast address (n_images = 1) that the NVSwitch delivers to every rank
- * (multimem.st).  Rows outside [row0, row0 + nrow) are not touched; the caller orders
- * the ranks (e.g. a symmetric-memory barrier) before reading.  No chirp split.
+/* Back-projection with the image gather (or the chirp-shard reduction) fused into the
+ * epilogue (NEXT-4; the north star's multi-GPU design): the same computation as
+ * sar_backproject for rows [row0, row0 + nrow) and chirps [chirp0, chirp0 + nchirp), but every
+ * finished tile goes to its ABSOLUTE rows row0 + j of each full image images[d] (complex
+ * [ny][nx], d < n_images <= 8) while the remaining tiles are still being computed:
+ *   flags = 0                   store (pixel-row shards: the gather)
+ *   flags |= SAR_SCATTER_ADD    atomic add (chirp shards: the reduction; images must hold the
+ *                               running sum, e.g. zeroed before the first shard)
+ *   flags |= SAR_SCATTER_MULTICAST  images[0] is an NVSwitch multicast address (n_images = 1):
+ *                               multimem.st / multimem.red reach every rank's image at once
+ * With symmetric memory the images are the P2P-mapped buffers of every rank (one NVLink
+ * store or reduction per peer).  Rows outside [row0, row0 + nrow) are not touched; the caller
+ * orders the ranks (e.g. a symmetric-memory barrier) before reading.  No chirp split.
  *   images  host array of n_images device pointers (may be peer or multicast addresses) */
+#define SAR_SCATTER_MULTICAST 1
+#define SAR_SCATTER_ADD 2
 sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* profiles,
                                      const double* tx_pos, const double* rx_pos,
                                      const float* doppler_bins, int32_t chirp0, int32_t nchirp,
                                      int32_t row0, int32_t nrow, sar_complex64_t* const* images,
-                                     int32_t n_images, int32_t multicast, sar_stream_t stream);
+                                     int32_t n_images, int32_t flags, sar_stream_t stream);
 
 /* End-to-end image formation from HOST buffers (the paper's "Load" + "BP",
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a

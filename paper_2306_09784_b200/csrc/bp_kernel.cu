@@ -594,11 +594,23 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         // over NVLink while other tiles are still being computed
         const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
         if (a.multicast) {
-          asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(a.peer[0] + o),
-                       "f"(acc_r[p]), "f"(acc_i[p])
-                       : "memory");
+          float* d = reinterpret_cast<float*>(a.peer[0] + o);
+          if (a.accumulate) {   // chirp shards: the NVSwitch adds into every rank's image
+            asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+            asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+          } else {
+            asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(d), "f"(acc_r[p]),
+                         "f"(acc_i[p])
+                         : "memory");
+          }
+        } else if (a.accumulate) {   // chirp shards: P2P reductions into the peers' images
+          for (int q = 0; q < a.n_peer; ++q) {
+            float* d = reinterpret_cast<float*>(a.peer[q] + o);
+            asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+            asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+          }
         } else {
-          for (int d = 0; d < a.n_peer; ++d) a.peer[d][o] = make_float2(acc_r[p], acc_i[p]);
+          for (int q = 0; q < a.n_peer; ++q) a.peer[q][o] = make_float2(acc_r[p], acc_i[p]);
         }
       } else if (a.ksplit > 1) {
         // several chirp chunks add into the same pixel (the image was zeroed first when

@@ -559,16 +559,18 @@ sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* pro
                                      const double* tx_pos, const double* rx_pos,
                                      const float* doppler_bins, int32_t chirp0, int32_t nchirp,
                                      int32_t row0, int32_t nrow, sar_complex64_t* const* images,
-                                     int32_t n_images, int32_t multicast, sar_stream_t stream) {
+                                     int32_t n_images, int32_t flags, sar_stream_t stream) {
   if (!images || n_images < 1 || n_images > 8)
     return fail(SAR_ERR_INVALID_ARGUMENT, "images must hold 1..8 device pointers");
-  if (multicast != 0 && multicast != 1) return fail(SAR_ERR_INVALID_ARGUMENT, "multicast must be 0 or 1");
+  if (flags & ~(SAR_SCATTER_MULTICAST | SAR_SCATTER_ADD)) return fail(SAR_ERR_INVALID_ARGUMENT, "unknown flags");
+  const int multicast = (flags & SAR_SCATTER_MULTICAST) ? 1 : 0, add = (flags & SAR_SCATTER_ADD) ? 1 : 0;
   if (multicast && n_images != 1)
     return fail(SAR_ERR_INVALID_ARGUMENT, "a multicast store takes exactly one (multicast) address");
   for (int d = 0; d < n_images; ++d)
     if (!images[d]) return fail(SAR_ERR_INVALID_ARGUMENT, "null image pointer");
+  if (add && nchirp == 0) return SAR_OK;
   return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, row0, nrow, images[0],
-                          0, images, n_images, multicast, stream);
+                          add, images, n_images, multicast, stream);
 }
 
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,

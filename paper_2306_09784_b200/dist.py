@@ -77,7 +77,8 @@ class FusedRowGather:
 
     ``ptrs`` are the P2P-mapped buffers of all ranks (``multicast=False``) or the single
     multicast address (``multicast=True``, when the NVSwitch supports it and
-    ``prefer_multicast``).  After the scatter launch, ``barrier()`` orders every rank's
+    ``prefer_multicast``).  ``root_ptrs`` addresses rank ``root``'s buffer only (the fused
+    chirp-shard reduction).  After the scatter launch, ``barrier()`` orders every rank's
     stores before any rank reads ``image``."""
 
     def __init__(self, ny: int, nx: int, device, group=None, prefer_multicast: bool = True):
@@ -94,6 +95,9 @@ class FusedRowGather:
         self.image = torch.view_as_complex(self.buf.view(ny, nx, 2))
         self.multicast = bool(prefer_multicast and self.hdl.multicast_ptr)   # 0 without NVLS multicast
         self.ptrs = [int(self.hdl.multicast_ptr)] if self.multicast else [int(p) for p in self.hdl.buffer_ptrs]
+
+    def root_ptrs(self, root: int = 0):
+        return [int(self.hdl.buffer_ptrs[root])]
 
     def barrier(self, channel: int = 0):
         self.hdl.barrier(channel=channel)

@@ -181,11 +181,15 @@ def sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row
                                   img_ptr, accumulate, stream))
 
 
+SAR_SCATTER_MULTICAST = 1
+SAR_SCATTER_ADD = 2
+
+
 def sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow, image_ptrs,
-                            multicast=0, stream=0):
+                            flags=0, stream=0):
     arr = (_vp * len(image_ptrs))(*image_ptrs)
     _check(load().sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow,
-                                          arr, len(image_ptrs), int(multicast), stream))
+                                          arr, len(image_ptrs), int(flags), stream))
 
 
 def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream=0):
@@ -374,10 +378,11 @@ class Plan:
         return out
 
     def backproject_scatter(self, profiles, tx, image_ptrs, rx=None, doppler=None, chirp0=0, nchirp=None, row0=0,
-                            nrow=None, multicast=False, stream=None):
-        """Back-project rows [row0, row0+nrow) and store each finished tile at its absolute rows of
-        every full image in ``image_ptrs`` (device addresses: local, P2P-mapped peer buffers, or
-        one multicast address with ``multicast=True``) -- the gather fused into the epilogue."""
+                            nrow=None, multicast=False, add=False, stream=None):
+        """Back-project rows [row0, row0+nrow) and store (``add``: atomically add) each finished tile
+        at its absolute rows of every full image in ``image_ptrs`` (device addresses: local,
+        P2P-mapped peer buffers, or one multicast address with ``multicast=True``) -- the gather
+        (or the chirp-shard reduction) fused into the epilogue."""
         import torch
 
         nchirp = self.n_chirps - chirp0 if nchirp is None else nchirp
@@ -387,7 +392,8 @@ class Plan:
                                 _dptr(tx, torch.float64, (self.n_chirps, 3), "tx"),
                                 _dptr(rx, torch.float64, (self.n_chirps, self.n_rx, 3), "rx"),
                                 _dptr(doppler, torch.float32, (self.grid.ny, self.grid.nx), "doppler"),
-                                chirp0, nchirp, row0, nrow, [int(p) for p in image_ptrs], int(bool(multicast)),
+                                chirp0, nchirp, row0, nrow, [int(p) for p in image_ptrs],
+                                (SAR_SCATTER_MULTICAST if multicast else 0) | (SAR_SCATTER_ADD if add else 0),
                                 _stream_handle(stream))
 
     def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, row0=0, nrow=None, out_h=None,
