@@ -400,7 +400,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": scn.updates / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_image": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "sar_form_image (C ABI, pinned host buffers: H2D raw+poses, rc, bp, D2H image rows)"},
+                    "api": "sar_form_image (C ABI, pinned host buffers: H2D raw+poses, rc, bp whose epilogue "
+                           "stores the image rows into the mapped pinned host buffer)"},
             "gpu_launches": launches,
             "clocks": clocks,
         }

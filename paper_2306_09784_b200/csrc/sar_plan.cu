@@ -626,6 +626,20 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   st = sar_range_compress(plan, plan->w_raw, w_sar_host ? plan->w_wsar : nullptr, 0, r.n_chirps,
                           reinterpret_cast<sar_complex64_t*>(plan->w_prof), stream);
   if (st != SAR_OK) return st;
+  // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
+  // under UVA) and the shard is large enough to fill the GPU without a chirp split, every
+  // finished tile is stored straight into host memory while the other tiles compute; else
+  // one device->host copy after the kernel.
+  void* mapped = nullptr;
+  const bool direct = nrow > 0 && (int64_t)nrow * g.nx >= ((int64_t)1 << 20) &&
+                      cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;
+  if (!direct) cudaGetLastError();   // clear the error of a pageable buffer
+  if (direct) {
+    sar_complex64_t* base = reinterpret_cast<sar_complex64_t*>(mapped) - (ptrdiff_t)row0 * g.nx;
+    return backproject_impl(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
+                            rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0, r.n_chirps,
+                            row0, nrow, base, 0, &base, 1, 0, stream);
+  }
   st = sar_backproject(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
                        rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0,
                        r.n_chirps, row0, nrow, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, stream);

@@ -310,6 +310,30 @@ def test_form_image_host_buffers_equal_device_path(cuda_lib):
     plan.close()
 
 
+@pytest.mark.parametrize("rows", [(0, 1200), (100, 700)])
+def test_form_image_direct_host_stores_equal_device_path(cuda_lib, rows):
+    """Large shards of a pinned host image take the fused readback (the BP epilogue stores
+    into mapped host memory); pageable host images take the copy path.  Both equal the
+    device path bit for bit."""
+    import torch
+
+    scn = sarsim.make_config("C2", n_chirps=512)
+    raw = _raw(scn)
+    row0, nrow = rows
+    lo, hi = scn.antenna_box(1e-3)
+    plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, 1, (lo, hi))
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    ref = plan.backproject(plan.range_compress(raw), tx, row0=row0, nrow=nrow).cpu()
+    raw_h, tx_h = raw.cpu().pin_memory(), torch.as_tensor(scn.tx).pin_memory()
+    pinned = torch.full((nrow, scn.grid.nx), complex(5.0, 5.0), dtype=torch.complex64).pin_memory()
+    out = plan.form_image(raw_h, tx_h, row0=row0, nrow=nrow, out_h=pinned)
+    assert torch.equal(out, ref)
+    pageable = torch.empty((nrow, scn.grid.nx), dtype=torch.complex64)
+    out2 = plan.form_image(raw_h, tx_h, row0=row0, nrow=nrow, out_h=pageable)
+    assert torch.equal(out2, ref)
+    plan.close()
+
+
 # ----------------------------------------------------------------------------- C5 streaming
 def test_C5_streaming_frame_sampled_parity_and_chirp_shards(cuda_lib):
     """One C5 frame (chirps [f H, f H + 8192) of the long track, grid re-centred on the frame):
