@@ -209,9 +209,9 @@ sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* pro
  * plan-owned device workspace, runs sar_range_compress over all chirps and
  * sar_backproject over all chirps for grid rows [row0, row0 + nrow), and returns
  * those image rows, all on `stream`.  When image_host is pinned (device-mapped) and
- * the shard has >= 2^20 pixels, the BP epilogue stores each finished tile straight
- * into image_host (readback overlapped with the compute); otherwise one copy follows
- * the kernel.
+ * the shard fills the GPU without a chirp split, the BP epilogue stores each finished
+ * tile straight into image_host (readback overlapped with the compute); otherwise one
+ * copy follows the kernel.  A pinned raw_host is read by the range compression directly.
  *   raw_host [n_chirps][n_rx][n_samples] float; w_sar_host [n_chirps] float or NULL;
  *   tx_host [n_chirps][3] double; rx_host [n_chirps][n_rx][3] double or NULL;
  *   doppler_host [ny][nx] float or NULL; image_host [nrow][nx] complex (written).

@@ -698,7 +698,12 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
-  while (a.n_peer == 0 && ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
+  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
+  if (a.split_query) {   // planning query: the split a plain launch would use; nothing runs
+    *a.split_query = k;
+    return cudaSuccess;
+  }
+  if (a.n_peer > 0) k = 1;   // scatter epilogue: stores, no chirp split
   b.chunk = (a.nchirp + k - 1) / k;
   b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
   b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);

@@ -59,6 +59,7 @@ struct BpArgs {
   // written with multimem.st when multicast != 0) instead of img
   float2* peer[8];
   int n_peer, multicast;
+  int* split_query;        // non-null: report the chirp split of this launch, do not launch
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };

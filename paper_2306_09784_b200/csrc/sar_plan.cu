@@ -475,7 +475,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
                               const double* rx_pos, const float* doppler_bins, int32_t chirp0,
                               int32_t nchirp, int32_t row0, int32_t nrow, sar_complex64_t* image,
                               int32_t accumulate, sar_complex64_t* const* peers, int32_t n_peer,
-                              int32_t multicast, sar_stream_t stream) {
+                              int32_t multicast, sar_stream_t stream, int* split_query = nullptr) {
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   const sar_radar_params_t& r = plan->radar;
   const sar_grid_t& g = plan->grid;
@@ -537,11 +537,12 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.C3f = (float)(2.0 * sar::kPi * a.c2 / a.a1);
   a.n_peer = n_peer;
   a.multicast = multicast;
+  a.split_query = split_query;
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
-  plan->launches.fetch_add(1);
+  if (!split_query) plan->launches.fetch_add(1);
   return SAR_OK;
 }
 }  // namespace
@@ -614,7 +615,15 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  if ((e = cudaMemcpyAsync(plan->w_raw, raw_host, M * R * NS * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+  // Raw samples are read exactly once, by the range compression: from a pinned (device-mapped)
+  // host buffer the kernel reads them over the host link directly (no staging copy); poses,
+  // re-read by every BP tile, are copied.
+  void* raw_mapped = nullptr;
+  const bool raw_direct = cudaHostGetDevicePointer(&raw_mapped, const_cast<float*>(raw_host), 0) == cudaSuccess &&
+                          raw_mapped;
+  if (!raw_direct) cudaGetLastError();
+  if ((!raw_direct &&
+       (e = cudaMemcpyAsync(plan->w_raw, raw_host, M * R * NS * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess) ||
       (e = cudaMemcpyAsync(plan->w_tx, tx_host, M * 3 * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync H2D");
   if (w_sar_host && (e = cudaMemcpyAsync(plan->w_wsar, w_sar_host, M * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -623,15 +632,21 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
     return cuda_fail(e, "cudaMemcpyAsync H2D");
   if (doppler_host && (e = cudaMemcpyAsync(plan->w_dop, doppler_host, npix * sizeof(float), cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync H2D");
-  st = sar_range_compress(plan, plan->w_raw, w_sar_host ? plan->w_wsar : nullptr, 0, r.n_chirps,
+  st = sar_range_compress(plan, raw_direct ? static_cast<const float*>(raw_mapped) : plan->w_raw,
+                          w_sar_host ? plan->w_wsar : nullptr, 0, r.n_chirps,
                           reinterpret_cast<sar_complex64_t*>(plan->w_prof), stream);
   if (st != SAR_OK) return st;
   // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
-  // under UVA) and the shard is large enough to fill the GPU without a chirp split, every
+  // under UVA) and the shard fills the GPU without a chirp split (asked of the launcher), every
   // finished tile is stored straight into host memory while the other tiles compute; else
   // one device->host copy after the kernel.
   void* mapped = nullptr;
-  const bool direct = nrow > 0 && (int64_t)nrow * g.nx >= ((int64_t)1 << 20) &&
+  int split = 0;
+  st = backproject_impl(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
+                        rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0, r.n_chirps, row0,
+                        nrow, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, nullptr, 0, 0, stream, &split);
+  if (st != SAR_OK) return st;
+  const bool direct = nrow > 0 && split == 1 &&
                       cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;
   if (!direct) cudaGetLastError();   // clear the error of a pageable buffer
   if (direct) {

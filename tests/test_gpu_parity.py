@@ -310,14 +310,15 @@ def test_form_image_host_buffers_equal_device_path(cuda_lib):
     plan.close()
 
 
-@pytest.mark.parametrize("rows", [(0, 1200), (100, 700)])
-def test_form_image_direct_host_stores_equal_device_path(cuda_lib, rows):
-    """Large shards of a pinned host image take the fused readback (the BP epilogue stores
-    into mapped host memory); pageable host images take the copy path.  Both equal the
-    device path bit for bit."""
+@pytest.mark.parametrize("cfg,rows", [("C3", (0, 3000)), ("C3", (96, 2000)), ("C2", (100, 700))])
+def test_form_image_direct_host_stores_equal_device_path(cuda_lib, cfg, rows):
+    """Shards that fill the GPU without a chirp split and a pinned host image take the fused
+    readback (the BP epilogue stores into mapped host memory; pinned raw samples are read by
+    the range compression in place); smaller shards and pageable images take the copy path.
+    All equal the device path bit for bit."""
     import torch
 
-    scn = sarsim.make_config("C2", n_chirps=512)
+    scn = sarsim.make_config(cfg, n_chirps=512)
     raw = _raw(scn)
     row0, nrow = rows
     lo, hi = scn.antenna_box(1e-3)
