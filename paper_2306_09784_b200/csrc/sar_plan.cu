@@ -219,8 +219,9 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   auto smem = [&](int cb_, int st) { return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic); };
   if (auto_cb) {
     cb = std::max(1, 32 / r->n_rx);
-    // wide windows: fewer chirps per stage so that a 2-stage ring leaves room for two CTAs
-    while (cb > 1 && smem(cb, 2) > 96 * 1024) cb /= 2;
+    // wide windows: fewer chirps per stage so that a 2-stage ring fits in the ~56 KB that four
+    // resident CTAs per SM can each have (C0, W = 59: 3 -> 4 CTAs per SM, 12.9 -> 11.7 ms)
+    while (cb > 1 && smem(cb, 2) > 56 * 1024) cb /= 2;
   }
   for (;;) {
     const size_t stage_bytes = smem(cb, 2) - smem(cb, 1);
