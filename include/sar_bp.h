@@ -20,7 +20,9 @@
  *   - Errors: every call returns a sar_status_t and never throws across the ABI;
  *     sar_last_error() gives a thread-local message for the last failure.
  *   - The plan is immutable after creation: concurrent calls on different streams
- *     with disjoint output buffers are allowed.
+ *     with disjoint output buffers are allowed -- except sar_form_image, whose
+ *     device workspace belongs to the plan: its calls on one plan must share one
+ *     stream (or be serialised by the caller).
  */
 #ifndef SAR_BP_H
 #define SAR_BP_H

@@ -38,6 +38,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "sar_internal.h"
@@ -680,11 +681,16 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   auto kern = BpKernel<BI, DOP, SAFE, NCW, PB>::fn;
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
-  static int configured_bytes = -1;
-  if ((int)L.total > configured_bytes) {
+  // the dynamic shared-memory opt-in is per device and per kernel instantiation
+  static std::atomic<int> configured_bytes[kMaxDevices];
+  int cur_dev = 0;
+  if (cudaGetDevice(&cur_dev) != cudaSuccess || cur_dev < 0 || cur_dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if ((int)L.total > configured_bytes[cur_dev].load()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
-    configured_bytes = (int)L.total;
+    int prev = configured_bytes[cur_dev].load();
+    while ((int)L.total > prev && !configured_bytes[cur_dev].compare_exchange_weak(prev, (int)L.total)) {
+    }
   }
   BpArgs b = a;
   b.tiles_y = (a.nrow + TY - 1) / TY;
@@ -694,8 +700,7 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   int resident = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, (NCW + 1) * 32, L.total);
   int sms = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
   while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;

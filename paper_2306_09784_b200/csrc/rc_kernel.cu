@@ -10,6 +10,8 @@
 // digit-reversed order and the epilogue gathers only the cropped bins, separates the two
 // real spectra, applies the centring ramp exp(+j 2 pi k t_c / N) and the scale, and
 // stores coalesced complex64 rows.  HBM traffic per row: 4 Ns bytes read, 8 n_bins written.
+#include <atomic>
+
 #include "sar_internal.h"
 
 namespace sar {
@@ -136,12 +138,14 @@ __global__ void __launch_bounds__(BLOCK) rc_kernel(const RcArgs a) {
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s) {
   constexpr int kBlock = 256;
   const size_t smem = (size_t)a.nfft * sizeof(float2);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<bool> configured[kMaxDevices];   // the opt-in is per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!configured[dev].load()) {
     cudaError_t e = cudaFuncSetAttribute(rc_kernel<kBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          16384 * (int)sizeof(float2));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[dev].store(true);
   }
   const int grid = (a.nrows + 1) / 2;
   rc_kernel<kBlock><<<grid, kBlock, smem, s>>>(a);

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "../../include/sar_bp.h"
 
@@ -17,6 +18,7 @@ constexpr double kPi = 3.14159265358979323846;
 // warp/lane -> pixel map).
 constexpr int kTileX = 32;
 constexpr int kBpMaxStages = 8;          // shared-memory ring depth limit
+constexpr int kMaxDevices = 64;          // per-device launch configuration caches
 
 // Range-compression kernel arguments (rc_kernel.cu).
 struct RcArgs {
@@ -111,7 +113,8 @@ struct sar_plan_s {
   float2* d_twiddle = nullptr;
   float2* d_ramp = nullptr;
   float2* d_binphase = nullptr;
-  // sar_form_image workspace (lazily allocated)
+  // sar_form_image workspace (lazily allocated under ws_mutex)
+  std::mutex ws_mutex;
   float* w_raw = nullptr;
   float* w_wsar = nullptr;
   double* w_tx = nullptr;

@@ -607,12 +607,18 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   const size_t M = r.n_chirps, R = r.n_rx, NS = r.n_samples, NB = plan->info.n_bins;
   const size_t npix = (size_t)g.nx * g.ny;
   sar_status_t st;
-  if (!plan->w_raw) {
+  std::lock_guard<std::mutex> ws_lock(plan->ws_mutex);
+  if (!plan->w_img) {   // w_img is allocated last: non-null means the whole workspace exists
     if ((st = dev_alloc(&plan->w_raw, M * R * NS)) != SAR_OK || (st = dev_alloc(&plan->w_wsar, M)) != SAR_OK ||
         (st = dev_alloc(&plan->w_tx, M * 3)) != SAR_OK || (st = dev_alloc(&plan->w_rx, M * R * 3)) != SAR_OK ||
         (st = dev_alloc(&plan->w_dop, npix)) != SAR_OK || (st = dev_alloc(&plan->w_prof, M * R * NB)) != SAR_OK ||
-        (st = dev_alloc(&plan->w_img, npix)) != SAR_OK)
+        (st = dev_alloc(&plan->w_img, npix)) != SAR_OK) {
+      cudaFree(plan->w_raw); cudaFree(plan->w_wsar); cudaFree(plan->w_tx); cudaFree(plan->w_rx);
+      cudaFree(plan->w_dop); cudaFree(plan->w_prof);
+      plan->w_raw = nullptr; plan->w_wsar = nullptr; plan->w_tx = nullptr; plan->w_rx = nullptr;
+      plan->w_dop = nullptr; plan->w_prof = nullptr; plan->w_img = nullptr;
       return st;
+    }
   }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
