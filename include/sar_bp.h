@@ -239,6 +239,11 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
                                const double q_ref[3], const double v_avg[3], float* doppler_bins,
                                sar_stream_t stream);
 
+/* The same table for the pixels of a Measure E polar grid (image layout [n_r][n_th]). */
+sar_status_t sar_doppler_table_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                     const double q_ref[3], const double v_avg[3], float* doppler_bins,
+                                     sar_stream_t stream);
+
 /* Incremental streaming (NEXT-2; continuous processing): with a
  * world-fixed grid, a frame over an aperture of n_partials hops is the sum of the hops'
  * partial images (each sar_backproject over one hop of chirps).  Writes

@@ -11,8 +11,17 @@ __global__ void doppler_kernel(const DopArgs a) {
   const long n = (long)a.nx * a.ny;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     const int ix = (int)(i % a.nx), iy = (int)(i / a.nx);
-    const double dx = a.x0 + ix * a.dx - a.q[0];
-    const double dy = a.y0 + iy * a.dy - a.q[1];
+    double px, py;
+    if (a.polar) {   // Measure E grid: (xc + r sin th, yc + r cos th), image [n_r][n_th]
+      const double rr = a.r0 + iy * a.dr, th = a.th0 + ix * a.dth;
+      px = a.x0 + rr * sin(th);
+      py = a.y0 + rr * cos(th);
+    } else {
+      px = a.x0 + ix * a.dx;
+      py = a.y0 + iy * a.dy;
+    }
+    const double dx = px - a.q[0];
+    const double dy = py - a.q[1];
     const double dz = a.z0 - a.q[2];
     const double r = sqrt(dx * dx + dy * dy + dz * dz);
     const double vr = r > 0.0 ? a.legs * (dx * a.v[0] + dy * a.v[1] + dz * a.v[2]) / r : 0.0;

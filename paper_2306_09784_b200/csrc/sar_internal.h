@@ -76,6 +76,8 @@ struct DopArgs {
   float* out;              // [ny][nx]
   double x0, y0, z0, dx, dy;
   int nx, ny;
+  int polar;               // 1: polar grid, centre (x0, y0, z0), (r0, dr, th0, dth); nx = n_th, ny = n_r
+  double r0, dr, th0, dth;
   double q[3], v[3];       // reference antenna position, average velocity
   double legs;             // 2: TX and RX legs
   double bins_per_mps;     // f0 / c / (fs / N): bins per m/s of radial speed

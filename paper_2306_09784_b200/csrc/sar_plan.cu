@@ -696,7 +696,7 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
     return fail(SAR_ERR_INVALID_ARGUMENT, "grid needs dx, dy > 0 and nx, ny >= 1");
   for (int k = 0; k < 3; ++k)
     if (!isfinite(q_ref[k]) || !isfinite(v_avg[k])) return fail(SAR_ERR_INVALID_ARGUMENT, "non-finite q_ref/v_avg");
-  sar::DopArgs a;
+  sar::DopArgs a{};
   a.out = doppler_bins;
   a.x0 = grid->x0;
   a.y0 = grid->y0;
@@ -705,6 +705,42 @@ sar_status_t sar_doppler_table(const sar_radar_params_t* radar, const sar_grid_t
   a.dy = grid->dy;
   a.nx = grid->nx;
   a.ny = grid->ny;
+  for (int k = 0; k < 3; ++k) {
+    a.q[k] = q_ref[k];
+    a.v[k] = v_avg[k];
+  }
+  a.legs = 2.0;
+  a.bins_per_mps = radar->f0_hz / sar::kLightSpeed / (radar->sample_rate_hz / radar->fft_len);
+  cudaError_t e = sar::launch_doppler(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "doppler table launch");
+  return SAR_OK;
+}
+
+sar_status_t sar_doppler_table_polar(const sar_radar_params_t* radar, const sar_polar_grid_t* grid,
+                                     const double q_ref[3], const double v_avg[3], float* doppler_bins,
+                                     sar_stream_t stream) {
+  if (!radar || !grid || !q_ref || !v_avg || !doppler_bins)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (!finite_pos(radar->f0_hz) || !finite_pos(radar->sample_rate_hz) || radar->fft_len < 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "f0_hz, sample_rate_hz and fft_len must be positive");
+  double lo[3], hi[3];
+  sar_grid_t stand_in;
+  sar_status_t st = polar_box(grid, lo, hi, &stand_in);
+  if (st != SAR_OK) return st;
+  for (int k = 0; k < 3; ++k)
+    if (!isfinite(q_ref[k]) || !isfinite(v_avg[k])) return fail(SAR_ERR_INVALID_ARGUMENT, "non-finite q_ref/v_avg");
+  sar::DopArgs a{};
+  a.out = doppler_bins;
+  a.x0 = grid->xc;
+  a.y0 = grid->yc;
+  a.z0 = grid->zc;
+  a.nx = grid->n_th;
+  a.ny = grid->n_r;
+  a.polar = 1;
+  a.r0 = grid->r0;
+  a.dr = grid->dr;
+  a.th0 = grid->th0;
+  a.dth = grid->dth;
   for (int k = 0; k < 3; ++k) {
     a.q[k] = q_ref[k];
     a.v[k] = v_avg[k];

@@ -87,6 +87,9 @@ def load() -> ctypes.CDLL:
             lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
                                               P(ctypes.c_double * 3), _vp, _vp]
             lib.sar_doppler_table.restype = ctypes.c_int
+            lib.sar_doppler_table_polar.argtypes = [P(RadarParams), P(PolarGrid), P(ctypes.c_double * 3),
+                                                    P(ctypes.c_double * 3), _vp, _vp]
+            lib.sar_doppler_table_polar.restype = ctypes.c_int
             lib.sar_plan_create_polar.argtypes = [P(RadarParams), P(PolarGrid), P(Box), _i32, P(_vp)]
             lib.sar_plan_geometry_polar.argtypes = [P(RadarParams), P(PolarGrid), P(Box), P(PlanInfo)]
             lib.sar_polar_to_cartesian.argtypes = [P(PolarGrid), _vp, P(Grid), _vp, _vp]
@@ -211,13 +214,25 @@ def doppler_bound_bins(radar, v_avg) -> float:
     return 2.0 * radar.f0_hz * speed / 299792458.0 * radar.fft_len / radar.sample_rate_hz
 
 
+def sar_doppler_table_polar(radar: RadarParams, grid: PolarGrid, q_ref, v_avg, dop_ptr, stream=0):
+    q = (ctypes.c_double * 3)(*[float(v) for v in q_ref])
+    v = (ctypes.c_double * 3)(*[float(x) for x in v_avg])
+    _check(load().sar_doppler_table_polar(ctypes.byref(radar), ctypes.byref(grid), ctypes.byref(q), ctypes.byref(v),
+                                          dop_ptr, stream))
+
+
 def doppler_table(radar, grid, q_ref, v_avg, device=0, out=None, stream=None):
-    """Measure D table (float32 [ny][nx], CUDA) via sar_doppler_table."""
+    """Measure D table (float32 [ny][nx], CUDA) via sar_doppler_table (polar grids: [n_r][n_th]
+    via sar_doppler_table_polar)."""
     import torch
 
     out = torch.empty((grid.ny, grid.nx), dtype=torch.float32, device=f"cuda:{device}") if out is None else out
-    sar_doppler_table(radar_params(radar, 1, 1), grid_params(grid), q_ref, v_avg,
-                      _dptr(out, torch.float32, (grid.ny, grid.nx), "doppler"), _stream_handle(stream))
+    ptr = _dptr(out, torch.float32, (grid.ny, grid.nx), "doppler")
+    if hasattr(grid, "n_th"):
+        sar_doppler_table_polar(radar_params(radar, 1, 1), polar_grid_params(grid), q_ref, v_avg, ptr,
+                                _stream_handle(stream))
+    else:
+        sar_doppler_table(radar_params(radar, 1, 1), grid_params(grid), q_ref, v_avg, ptr, _stream_handle(stream))
     return out
 
 
