@@ -40,6 +40,14 @@ WORKLOADS = {
 }
 
 
+# The paper's own numbers for the same workload (Table 2; GTX 1080 Ti, BP kernel time):
+# context, not the target -- another machine.
+PAPER_UPD_S = {
+    "C6": (4.11e10, "paper Table 2 row 6 (P:L275-277): 1201^2 px x 1024 x 8 RX in 287.3 ms BP, GTX 1080 Ti"),
+    "C6p": (8.72e10, "paper Table 2 row 8 (P:L284-286): 165,061 px x 1024 x 8 RX in 15.5 ms BP, GTX 1080 Ti"),
+}
+
+
 def _env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -382,7 +390,9 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": (value / PAPER_UPD_S[args.config][0]) if args.config in PAPER_UPD_S else None,
+            "baseline_note": PAPER_UPD_S[args.config][1] if args.config in PAPER_UPD_S else None,
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "config": args.config, "pixels": g.nx * g.ny,
                        "chirps": scn.n_chirps, "n_rx": scn.n_rx, "samples": scn.radar.n_samples,
                        "fft_len": scn.radar.fft_len, "n_bins": plan.n_bins, "updates": scn.updates,
