@@ -437,3 +437,17 @@ def test_full_size_config_sampled_parity(cuda_lib, cfg):
         r = np.sort(np.abs(ref[sel]))
         if r[-1] > (1 + 4e-3) * r[-2]:
             assert np.argmax(np.abs(got[sel])) == np.argmax(np.abs(ref[sel]))
+
+
+@pytest.mark.parametrize("shape", ["4,4", "4,8", "8,8", "8,4,2,8", "8,4,5,4"])
+@pytest.mark.parametrize("n_rx", [1, 3])
+def test_cta_shapes_and_rings_match_oracle(cuda_lib, shape, n_rx, monkeypatch):
+    """Every supported CTA shape / ring configuration (SAR_BP_SHAPE="ncw,pb[,stages,cb]", the
+    tuning override; 4,4 is also the default of wide-window polar plans) meets the parity bar."""
+    monkeypatch.setenv("SAR_BP_SHAPE", shape)
+    scn = sarsim.small_config(n_chirps=72, ns=256, nx=70, ny=45, n_rx=n_rx, curved=n_rx > 1, seed=61)
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    assert rel_err(got, ref) <= REL_TOL
