@@ -5,11 +5,14 @@
 //   * One CTA = one 32 x (NCW*PB) pixel tile.  The tile anchor P_T is the tile centre (fp64).
 //   * Warp NCW is the PRODUCER: for each ring stage of CB chirps it computes, in fp64,
 //     the per-(tile, chirp, antenna) anchor record (D = P_T - q, r = |D|, anchor index
-//     and anchor phase) and stages the W profile bins the tile can touch for that chirp
-//     into shared memory in "pair" format {mid = (X[k]+X[k+1])/2, diff = X[k+1]-X[k]},
-//     so that linear interpolation is one LDS.128 plus two FFMA.  The window bound is
-//     the triangle inequality |d_hyp - d_anchor| <= 2 rho_T, valid for ANY track and
-//     chirp order (no fallback path).
+//     and anchor phase) and stages the W profile entries the tile can touch for that chirp
+//     into shared memory in "pair" format {mid = (X[k]+X[k+1])/2, diff = X[k+1]-X[k]} x
+//     carrier bin phase, so that linear interpolation is one LDS.128 plus two FFMA.  The
+//     entries come from pair-format rows built once per chirp row (pair_kernel) with one
+//     1-D bulk copy (TMA engine) per item; without that workspace the producer builds them
+//     itself from the profiles (same values; the path used if the rows cannot be allocated).
+//     The window bound is the triangle inequality |d_hyp - d_anchor| <= 2 rho_T (tighter
+//     for polar tiles), valid for ANY track and chirp order.
 //   * Warps 0..NCW-1 are CONSUMERS: each thread owns PB pixels (register accumulators);
 //     for one register slot a warp's 32 lanes cover an 8x4 pixel patch, so their gathers
 //     hit few distinct bins (broadcast, no bank conflicts).
@@ -109,6 +112,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+      "r"(bytes)
+      : "memory");
+}
+// 1-D bulk copy global -> shared on the TMA engine; completion counted in bytes on an mbarrier.
+// dst, src 16-B aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
 
@@ -343,9 +362,30 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         srec[2 * ri] = leg0;
         srec[2 * ri + 1] = make_float4(NEAR ? (float)(dz * dz) : 0.f,
                                        (float)(kap - k0 - 0.5 - wh), 0.f, __uint_as_float(off));
-        skw[e] = make_int2(k0, (m * a.n_rx + n) * a.n_bins);
+        skw[e] = make_int2(k0, a.pairs ? (m * a.n_rx + n) : (m * a.n_rx + n) * a.n_bins);
       }
       __syncwarp();
+      if (a.pairs) {
+        // bulk copies of pair-format rows: lane 0 adds the stage's byte count to the full
+        // barrier, every lane arrives after issuing its copies; a start outside the padded row
+        // (antennas outside the declared box) is clamped: wrong values, never out of bounds
+        if (lane == 0) mbar_arrive_expect_tx(bar_full + 8 * slot, (uint32_t)items * a.W * 16u);
+        __syncwarp();
+        const uint32_t wdst = smem_u32(swin);
+        for (int e = lane; e < items; e += 32) {
+          const int2 kw = skw[e];
+          const int i0 = min(max(kw.x + a.pair_pad, 0), a.pair_stride - a.W);
+          bulk_g2s(wdst + 16u * (uint32_t)(e * a.W), a.pairs + (size_t)kw.y * a.pair_stride + i0, 16u * a.W,
+                   bar_full + 8 * slot);
+        }
+        if (lane != 0) mbar_arrive(bar_full + 8 * slot);
+        SAR_TR(8, it, 2);
+        if (++slot == S) {
+          slot = 0;
+          parity ^= 1;
+        }
+        continue;
+      }
       // ---- profile windows in pair format: lane j of an item produces entry j from bins
       //      k0+j and k0+j+1 (the latter from lane j+1 by shuffle); kBatch rows in flight
       for (int j0w = 0; j0w < a.W; j0w += 31) {

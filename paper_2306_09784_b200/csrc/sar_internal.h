@@ -62,6 +62,8 @@ struct BpArgs {
   float2* peer[8];
   int n_peer, multicast;
   int* split_query;        // non-null: report the chirp split of this launch, do not launch
+  const float4* pairs;     // pair-format rows [n_chirps * n_rx][pair_stride] (pair_kernel) or nullptr
+  int pair_stride, pair_pad;
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };
@@ -96,6 +98,15 @@ struct ResampleArgs {
 };
 cudaError_t launch_resample(const ResampleArgs& a, cudaStream_t s);
 
+// Pair-format rows for the BP producer's bulk copies (pair_kernel.cu).
+struct PairArgs {
+  const float2* prof;      // [rows][n_bins]
+  const float2* binphase;  // [n_bins + 1], from k = -1
+  float4* out;             // [rows][stride]
+  int row0, rows, n_bins, stride, pad;
+};
+cudaError_t launch_pairs(const PairArgs& a, cudaStream_t s);
+
 }  // namespace sar
 
 struct sar_plan_s {
@@ -124,5 +135,6 @@ struct sar_plan_s {
   float* w_dop = nullptr;
   float2* w_prof = nullptr;
   float2* w_img = nullptr;
+  cudaMemPool_t pool = nullptr;   // device pool of the per-call pair-format rows (not owned)
   std::atomic<int64_t> launches{0};
 };

@@ -286,6 +286,7 @@ void free_plan(sar_plan_s* p) {
   cudaFree(p->d_twiddle);
   cudaFree(p->d_ramp);
   cudaFree(p->d_binphase);
+
   cudaFree(p->w_raw);
   cudaFree(p->w_wsar);
   cudaFree(p->w_tx);
@@ -386,6 +387,33 @@ static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_
   p->bp_ncw = d.ncw;
   p->bp_pb = d.pb;
   p->bp_stages = d.stages;
+  {
+    // per-device pool for the per-call pair-format rows: stream-ordered allocations that stay
+    // warm across calls and plans (C5's frame plans share it); created once, never released
+    static std::mutex pool_mutex;
+    static cudaMemPool_t pools[sar::kMaxDevices] = {};
+    std::lock_guard<std::mutex> lock(pool_mutex);
+    if (device >= sar::kMaxDevices) {
+      free_plan(p);
+      return fail(SAR_ERR_UNSUPPORTED_DEVICE, "device index too large");
+    }
+    if (!pools[device]) {
+      cudaMemPoolProps pp{};
+      pp.allocType = cudaMemAllocationTypePinned;
+      pp.handleTypes = cudaMemHandleTypeNone;
+      pp.location.type = cudaMemLocationTypeDevice;
+      pp.location.id = device;
+      cudaError_t e = cudaMemPoolCreate(&pools[device], &pp);
+      if (e != cudaSuccess) {
+        pools[device] = nullptr;
+        free_plan(p);
+        return cuda_fail(e, "cudaMemPoolCreate");
+      }
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    p->pool = pools[device];
+  }
 
   // Constant tables, computed in double and rounded once to float32.
   const int ns = radar->n_samples, N = radar->fft_len, nb = d.info.n_bins;
@@ -552,11 +580,53 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.n_peer = n_peer;
   a.multicast = multicast;
   a.split_query = split_query;
+  a.pairs = nullptr;
+  a.pair_stride = a.pair_pad = 0;
+  float4* pairs = nullptr;
+  static const bool no_pairs = [] {   // test switch: the producer builds the windows itself
+    const char* e = getenv("SAR_BP_NO_PAIRS");
+    return e && e[0] == '1';
+  }();
+  if (nchirp > 0 && !split_query && !no_pairs) {
+    // Pair-format rows of this call's chirps (pair_kernel, HBM-bound), in a stream-ordered
+    // allocation from the plan's pool so that calls on different streams stay independent;
+    // the BP producer then only issues one bulk copy per (tile, chirp, RX) window.
+    const int pad = plan->info.window_bins + 2, stride = plan->info.n_bins + 2 * pad;
+    const size_t rows = (size_t)nchirp * r.n_rx;
+    cudaError_t pe = cudaMallocFromPoolAsync((void**)&pairs, rows * stride * sizeof(float4), plan->pool,
+                                             (cudaStream_t)stream);
+    if (pe != cudaSuccess) {   // no room for the rows: the producer builds the windows itself
+      cudaGetLastError();
+      pairs = nullptr;
+    }
+  }
+  if (pairs) {
+    const int pad = plan->info.window_bins + 2, stride = plan->info.n_bins + 2 * pad;
+    const size_t rows = (size_t)nchirp * r.n_rx;
+    sar::PairArgs pa;
+    pa.prof = a.prof + (size_t)chirp0 * r.n_rx * plan->info.n_bins;
+    pa.binphase = plan->d_binphase;
+    pa.out = pairs;
+    pa.row0 = 0;
+    pa.rows = (int)rows;
+    pa.n_bins = plan->info.n_bins;
+    pa.stride = stride;
+    pa.pad = pad;
+    cudaError_t pe = sar::launch_pairs(pa, (cudaStream_t)stream);
+    if (pe != cudaSuccess) {
+      cudaFreeAsync(pairs, (cudaStream_t)stream);
+      return cuda_fail(pe, "pair-format launch");
+    }
+    a.pairs = pairs - (size_t)chirp0 * r.n_rx * stride;   // indexed by absolute (chirp, RX) row
+    a.pair_stride = stride;
+    a.pair_pad = pad;
+  }
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
+  if (pairs) cudaFreeAsync(pairs, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
-  if (!split_query) plan->launches.fetch_add(1);
+  if (!split_query) plan->launches.fetch_add(pairs ? 2 : 1);
   return SAR_OK;
 }
 }  // namespace

@@ -451,3 +451,25 @@ def test_cta_shapes_and_rings_match_oracle(cuda_lib, shape, n_rx, monkeypatch):
     ref = oracle_image(scn, raw.cpu().numpy())
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
     assert rel_err(got, ref) <= REL_TOL
+
+
+def test_producer_built_windows_match_pair_rows(cuda_lib, monkeypatch):
+    """The BP producer's own window construction (used when the pair-format rows cannot be
+    allocated; forced here with SAR_BP_NO_PAIRS=1 in a fresh process) gives the same image."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, torch, sarsim\n"
+            "from tests.helpers import gpu_image\n"
+            "scn = sarsim.small_config(n_chirps=80, ns=256, nx=70, ny=45, n_rx=2, curved=True, seed=62)\n"
+            "raw = sarsim.simulate_raw(scn, device='cuda:0')\n"
+            "np.save(sys.argv[1], gpu_image(scn, raw).cpu().numpy())\n") % os.getcwd()
+    outs = []
+    for flag in ("0", "1"):
+        path = f"/tmp/_sar_np_{os.getpid()}_{flag}.npy"
+        env = dict(os.environ, SAR_BP_NO_PAIRS=flag)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env)
+        outs.append(np.load(path))
+    # same per-entry arithmetic in both places; allow FMA-contraction differences
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-6 * np.abs(outs[0]).max()
