@@ -130,3 +130,16 @@ def test_plan_create_without_gpu_reports_device_error(lib):
     with pytest.raises(sar.SarError) as e:
         sar.sar_plan_create(rp, gp, bp, 0)
     assert e.value.status in (3, 5)
+
+
+def test_bp_kernel_sass_uses_bulk_copies_packed_fp32_and_mbarriers():
+    """Blackwell-native evidence in the built library: the BP producer's 1-D bulk copies (TMA
+    engine, UBLKCP), the consumers' packed fp32 pairs (FFMA2), MUFU rsqrt/sin/cos and the
+    mbarrier ring (SYNCS) are all in bp_kernel's SASS."""
+    _build.build()
+    sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    bp = "".join(f for f in funcs if f.startswith("_ZN3sar") and "bp_kernel_mono" in f.split("\n", 1)[0])
+    assert bp, "bp_kernel_mono not found in libsar.so"
+    for mnemonic in ("UBLKCP", "FFMA2", "MUFU.RSQ", "MUFU.SIN", "MUFU.COS", "SYNCS.ARRIVE", "SYNCS.PHASECHK"):
+        assert mnemonic in bp, mnemonic
