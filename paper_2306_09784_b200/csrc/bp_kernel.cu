@@ -60,6 +60,10 @@ constexpr int kBatch = SAR_BP_BATCH;     // producer: profile rows loaded per ba
 #define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
 #endif
 constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
+#ifndef SAR_BP_RX_UNROLL
+#define SAR_BP_RX_UNROLL 4                // bistatic RX-loop unroll (C4 1146 -> 1112 ms; 2 is slower)
+#endif
+constexpr int kRxUnroll = SAR_BP_RX_UNROLL;
 // (A min-blocks launch bound, even "1", changes ptxas's schedule: measured 5 % slower on C3;
 //  capping registers for 6-7 resident CTAs spilled and was slower too.  tools/vsweep.sh)
 
@@ -538,7 +542,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 #pragma unroll
           for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
           const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
-#pragma unroll 1
+#pragma unroll kRxUnroll
           for (int n = 0; n < a.n_rx; ++n, rp += 2) {
             const float4 A = rp[0], B = rp[1];
 #pragma unroll
