@@ -60,6 +60,10 @@ constexpr int kBatch = SAR_BP_BATCH;     // producer: profile rows loaded per ba
 #define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
 #endif
 constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
+#ifndef SAR_BP_MIN_SPLIT
+#define SAR_BP_MIN_SPLIT 512               // chirp split: (chirp, RX) items per chunk at least
+#endif
+constexpr long kMinSplitItems = SAR_BP_MIN_SPLIT;
 #ifndef SAR_BP_RX_UNROLL
 #define SAR_BP_RX_UNROLL 4                // bistatic RX-loop unroll (C4 1146 -> 1112 ms; 2 is slower)
 #endif
@@ -747,7 +751,8 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
-  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= 512 && a.nchirp / (2 * k) >= a.CB) k *= 2;
+  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems && a.nchirp / (2 * k) >= a.CB)
+    k *= 2;
   if (a.split_query) {   // planning query: the split a plain launch would use; nothing runs
     *a.split_query = k;
     return cudaSuccess;
