@@ -473,3 +473,17 @@ def test_producer_built_windows_match_pair_rows(cuda_lib, monkeypatch):
         outs.append(np.load(path))
     # same per-entry arithmetic in both places; allow FMA-contraction differences
     assert np.abs(outs[0] - outs[1]).max() <= 1e-6 * np.abs(outs[0]).max()
+
+
+@pytest.mark.parametrize("shape", [None, "8,4,3,4"])
+def test_sixteen_rx_array_matches_oracle(cuda_lib, shape, monkeypatch):
+    """The paper's reference setup: 16 RX (Table 1; Measure F keeps 8).  With the override 4
+    chirps x 16 RX = 64 items share a ring stage (more items than producer lanes)."""
+    if shape:
+        monkeypatch.setenv("SAR_BP_SHAPE", shape)
+    scn = sarsim.small_config(n_chirps=40, ns=256, nx=45, ny=36, n_rx=16, seed=63)
+    raw = _raw(scn)
+    got = gpu_image(scn, raw).cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    assert rel_err(got, ref) <= REL_TOL
