@@ -487,3 +487,20 @@ def test_sixteen_rx_array_matches_oracle(cuda_lib, shape, monkeypatch):
     ref = oracle_image(scn, raw.cpu().numpy())
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
     assert rel_err(got, ref) <= REL_TOL
+
+
+def test_largest_fft_and_full_crop_match_oracle(cuda_lib):
+    """Maximum transform size (fft_len = 16384, Ns = 2048: 128 KB of shared memory per FFT) and
+    the smallest range-bin spacing (Z = 8 over 2048 samples)."""
+    scn = sarsim.small_config(n_chirps=24, ns=2048, nx=40, ny=30, seed=64)
+    assert scn.radar.fft_len == 16384
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    ref_prof = oracle_profiles(scn, raw.cpu().numpy(), plan.k_lo, plan.n_bins)
+    got_prof = prof.cpu().numpy()
+    assert np.abs(got_prof - ref_prof).max() <= 1e-5 * np.abs(ref_prof).max()
+    got = img.cpu().numpy().reshape(-1)
+    ref = oracle_image(scn, raw.cpu().numpy())
+    plan.close()
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    assert rel_err(got, ref) <= REL_TOL
