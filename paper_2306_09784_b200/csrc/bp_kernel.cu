@@ -222,7 +222,8 @@ __device__ __forceinline__ float leg_delta(float D2x, float D2y, float r2, float
 }
 
 // The far-field leg for a pixel pair (FFMA2 form of leg_delta<false>); record
-// A = {2Dx, 2Dy, r^2, r}.
+// A = {2Dx, 2Dy, r^2, r}; the second record word is B = {kappa_anchor, window address,
+// Dz^2 (near field), 0}, so the consumer reads (kappa_anchor, address) with one LDS.64.
 __device__ __forceinline__ f32x2 leg_delta2(const float4 A, const f32x2 UX, const f32x2 UY, const f32x2 W) {
   const f32x2 G2 = ffma2(bc2(A.x), UX, ffma2(bc2(A.y), UY, W));   // 2 D.u + |u|^2
   const f32x2 S = fadd2(G2, bc2(A.z));                            // ~|p - q|^2
@@ -330,7 +331,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
-          srec[2 * c + 1] = make_float4(NEAR ? (float)(Dz * Dz) : 0.f, 0.f, 0.f, 0.f);
+          srec[2 * c + 1] = make_float4(0.f, 0.f, NEAR ? (float)(Dz * Dz) : 0.f, 0.f);
         }
       }
       for (int e = lane; e < items; e += 32) {
@@ -368,8 +369,8 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         const uint32_t off = waddr + 16u * (uint32_t)wh - 16u * kMagicBits;
         const int ri = BISTATIC ? a.CB + e : e;
         srec[2 * ri] = leg0;
-        srec[2 * ri + 1] = make_float4(NEAR ? (float)(dz * dz) : 0.f,
-                                       (float)(kap - k0 - 0.5 - wh), 0.f, __uint_as_float(off));
+        srec[2 * ri + 1] = make_float4((float)(kap - k0 - 0.5 - wh), __uint_as_float(off),
+                                       NEAR ? (float)(dz * dz) : 0.f, 0.f);
         skw[e] = make_int2(k0, a.pairs ? (m * a.n_rx + n) : (m * a.n_rx + n) * a.n_bins);
       }
       __syncwarp();
@@ -536,7 +537,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         for (int c = 0; c < cnt; ++c) {
           const float4 A = srec[2 * c], B = srec[2 * c + 1];
 #pragma unroll
-          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.y, __float_as_uint(B.w));
+          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.x, __float_as_uint(B.y));
         }
       } else {
 #pragma unroll 1
@@ -551,7 +552,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             const float4 A = rp[0], B = rp[1];
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h)
-              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.y, __float_as_uint(B.w));
+              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.x, __float_as_uint(B.y));
           }
         }
       }
@@ -559,11 +560,11 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 #pragma unroll kChirpUnroll
       for (int c = 0; c < cnt; ++c) {
         const float4 A = srec[2 * c], B = srec[2 * c + 1];
-        const uint32_t off = __float_as_uint(B.w);
+        const uint32_t off = __float_as_uint(B.y);
 #pragma unroll
         for (int p = 0; p < PB; ++p) {
-          const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
-          float kap = fmaf(A1, dR, B.y);
+          const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+          float kap = fmaf(A1, dR, B.x);
           if (DOP) kap += fd[p];
           const float tk = kap + kMagic;
           const float kf = tk - kMagic;
@@ -584,16 +585,16 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         const float4 T = srec[2 * c], TB = srec[2 * c + 1];
         float dT[PB];
 #pragma unroll
-        for (int p = 0; p < PB; ++p) dT[p] = leg_delta<SAFE>(T.x, T.y, T.z, T.w, TB.x, ux[p], uy[p], wh[p]);
+        for (int p = 0; p < PB; ++p) dT[p] = leg_delta<SAFE>(T.x, T.y, T.z, T.w, TB.z, ux[p], uy[p], wh[p]);
 #pragma unroll 1
         for (int n = 0; n < a.n_rx; ++n) {
           const int ri = a.CB + c * a.n_rx + n;
           const float4 A = srec[2 * ri], B = srec[2 * ri + 1];
-          const uint32_t off = __float_as_uint(B.w);
+          const uint32_t off = __float_as_uint(B.y);
 #pragma unroll
           for (int p = 0; p < PB; ++p) {
-            const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.x, ux[p], uy[p], wh[p]);
-            float kap = fmaf(A1, dR, B.y);
+            const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+            float kap = fmaf(A1, dR, B.x);
             if (DOP) kap += fd[p];
             const float tk = kap + kMagic;
             const float kf = tk - kMagic;
