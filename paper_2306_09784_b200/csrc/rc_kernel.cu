@@ -10,8 +10,12 @@
 // digit-reversed order and the epilogue gathers only the cropped bins, separates the two
 // real spectra, applies the centring ramp exp(+j 2 pi k t_c / N) and the scale, and
 // stores coalesced complex64 rows.  HBM traffic per row: 4 Ns bytes read, 8 n_bins written.
+#include <stdlib.h>
+
+#include <algorithm>
 #include <atomic>
 
+#include "ptx_util.h"
 #include "sar_internal.h"
 
 namespace sar {
@@ -152,7 +156,254 @@ __global__ void __launch_bounds__(BLOCK) rc_kernel(const RcArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// rc_kernel_warp: the zero-padded transform as Zp = N / L transforms of length L (register
+// path, L in {256, 512}, Ns <= L).  With x[t] = 0 for t >= L,
+//   Z[Zp a + b] = sum_{t<L} (z[t] W_N^(b t)) W_L^(a t),      a < L, b < Zp,
+// so warp b computes one L-point FFT of the pre-twiddled row pair entirely in registers,
+// exchanging values between its radix-8 (last: radix-4 for L = 256) Stockham stages through
+// its own row of shared memory with warp-level synchronisation only; the rows are then the
+// b-major spectrum Z[Zp a + b] = Xs[b][a] the epilogue gathers the crop from.  One block-wide
+// barrier per row pair (the classic kernel has one per radix-4 pass); shared-memory traffic
+// per row pair about halves.  Numerically the same transform (fp32, fp64-built twiddles).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mj(float2 a) { return make_float2(a.y, -a.x); }   // a * (-j)
+
+// forward 4-point DFT, natural order in and out
+__device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
+  const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_mj(csub(a1, a3));
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, d13);
+  a3 = csub(d02, d13);
+}
+
+// forward R-point DFT (R = 4 or 8) of v[0..R), natural order in and out
+template <int R>
+__device__ __forceinline__ void dft(float2* v) {
+  if (R == 4) {
+    dft4(v[0], v[1], v[2], v[3]);
+  } else {
+    constexpr float c = 0.70710678118654752f;
+    // radix-2 split: even outputs from v[r] + v[r+4], odd outputs from (v[r] - v[r+4]) W_8^r
+    float2 e[4], o[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      e[r] = cadd(v[r], v[r + 4]);
+      o[r] = csub(v[r], v[r + 4]);
+    }
+    o[1] = make_float2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));    // * (c, -c)
+    o[2] = mul_mj(o[2]);                                                  // * -j
+    o[3] = make_float2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));   // * (-c, -c)
+    dft4(e[0], e[1], e[2], e[3]);
+    dft4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      v[2 * m] = e[m];
+      v[2 * m + 1] = o[m];
+    }
+  }
+}
+
+// physical index of entry i in a warp's row: one pad entry per 8 (conflict-free stride-8
+// stage-0 stores and split-run stage-1 stores for 8-byte elements)
+__device__ __forceinline__ int rpos(int i) { return i + (i >> 3); }
+
+template <int L>
+struct RcWarpPlan {
+  static constexpr int E = L / 32;                 // values per lane
+  static constexpr int RS = L + L / 8 + 2;         // row stride (complex): rows of different b
+                                                   // start in different bank pairs
+};
+
+// One radix-R Stockham stage over a warp's row (NS = product of the radices before it):
+// butterfly j takes in[j + r L/R], twiddles by W_(NS R)^((j mod NS) r) (table stw[k][R]),
+// and writes its natural-order outputs to (j / NS) NS R + (j mod NS) + r NS.  Lane addresses
+// are one base per butterfly plus compile-time offsets (rpos(i + 8 m) = rpos(i) + 9 m).
+template <int L, int R, int NS>
+__device__ __forceinline__ void stockham_stage(float2* v, float2* row, const float2* __restrict__ stw, int lane) {
+  constexpr int B = L / (32 * R);                  // butterflies per lane
+  static_assert((L / R) % 8 == 0 && NS % 8 == 0, "stage offsets must be multiples of 8");
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const float2* src = row + rpos(lane + 32 * s);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[s * R + r] = src[r * (L / R) * 9 / 8];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const int j = lane + 32 * s;
+    const int k = j % NS;
+    const float4* w4 = reinterpret_cast<const float4*>(stw + k * R);
+#pragma unroll
+    for (int h = 0; h < R / 2; ++h) {
+      const float4 w = __ldg(w4 + h);
+      if (h) v[s * R + 2 * h] = cmul(v[s * R + 2 * h], make_float2(w.x, w.y));
+      v[s * R + 2 * h + 1] = cmul(v[s * R + 2 * h + 1], make_float2(w.z, w.w));
+    }
+    dft<R>(v + s * R);
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const int j = lane + 32 * s;
+    float2* dst = row + rpos((j / NS) * NS * R + (j % NS));
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[r * NS * 9 / 8] = v[s * R + r];
+  }
+  __syncwarp();
+}
+
+// Persistent CTAs: CTA c transforms row pairs c, c + grid, ...; with RING > 0 the raw rows of
+// the next RING pairs are in flight into a shared-memory ring (one 1-D bulk copy of the pair's
+// contiguous 2 Ns floats per stage, mbarrier completion), so the transform of one pair overlaps
+// the HBM latency of the next ones.  RING = 0 reads the rows with plain loads (rows not 16-B
+// aligned, or raw samples in mapped host memory).
+template <int L, int WARPS, int RING>
+__global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? 3 : 1) rc_kernel_warp(const RcArgs a) {
+  extern __shared__ __align__(16) float2 xs[];   // [zp][RS] | raw ring [RING][2 ns] | mbarriers
+  constexpr int E = RcWarpPlan<L>::E, RS = RcWarpPlan<L>::RS;
+  const int N = a.nfft;
+  const int lzp = a.log2n - (L == 512 ? 9 : 8), zp = 1 << lzp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npairs = (a.nrows + 1) / 2;
+  float* ring = reinterpret_cast<float*>(xs + zp * RS);
+  const uint32_t bar0 = smem_u32(ring + RING * 2 * a.ns);
+  auto issue = [&](int pair, int slot) {   // one thread: the pair's raw rows -> ring slot
+    const int nr = min(2, a.nrows - 2 * pair);
+    const uint32_t bytes = (uint32_t)(nr * a.ns) * 4u;
+    mbar_arrive_expect_tx(bar0 + 8 * slot, bytes);
+    bulk_g2s(smem_u32(ring + slot * 2 * a.ns), a.raw + (size_t)(a.row0 + 2 * pair) * a.ns, bytes, bar0 + 8 * slot);
+  };
+  if (RING > 0) {
+    if (threadIdx.x == 0) {
+      for (int d = 0; d < RING; ++d) mbar_init(bar0 + 8 * d, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int d = 0; d < RING; ++d)
+        if (blockIdx.x + d * gridDim.x < npairs) issue(blockIdx.x + d * gridDim.x, d);
+    }
+    __syncthreads();
+  }
+
+  int it = 0;
+  for (int pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
+    const int ra = a.row0 + 2 * pair;
+    const bool has_b = 2 * pair + 1 < a.nrows;
+    const float* xa;
+    if (RING > 0) {
+      const int slot = it % RING;
+      mbar_wait(bar0 + 8 * slot, (uint32_t)(it / RING) & 1u);
+      xa = ring + slot * 2 * a.ns;
+    } else {
+      xa = a.raw + (size_t)ra * a.ns;
+    }
+    const float* xb = has_b ? xa + a.ns : xa;   // a lone last row reads row a again (unused)
+
+    for (int b = warp; b < zp; b += WARPS) {
+      float2 v[E];
+      float2* row = xs + b * RS;
+      const float2* cb = a.coef + (size_t)b * a.ns;
+      // stage 0 (radix 8, no twiddles), one butterfly at a time; inputs
+      // z[t] = c_b[t] (x_a[t] + j x_b[t]), c_b[t] = w[t] W_N^(b t), t = j + r L/8
+#pragma unroll 1
+      for (int s = 0; s < E / 8; ++s) {
+        const int j = lane + 32 * s;
+        // branch-free: all 24 loads of the butterfly are in flight together (a clamped index,
+        // then zero for t >= Ns)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int t = j + r * (L / 8);
+          const int tc = min(t, a.ns - 1);
+          const float2 c = __ldg(cb + tc);
+          const float va = RING > 0 ? xa[tc] : __ldg(xa + tc);
+          const float vb = has_b ? (RING > 0 ? xb[tc] : __ldg(xb + tc)) : 0.f;
+          const float2 z = make_float2(c.x * va - c.y * vb, c.x * vb + c.y * va);
+          v[r] = t < a.ns ? z : make_float2(0.f, 0.f);
+        }
+        dft<8>(v);
+        float2* dst = row + 9 * j;                 // rpos(8 j + r) = 9 j + r
+#pragma unroll
+        for (int r = 0; r < 8; ++r) dst[r] = v[r];
+      }
+      __syncwarp();
+      stockham_stage<L, 8, 8>(v, row, a.stw, lane);
+      stockham_stage<L, L / 64, 64>(v, row, a.stw + 64, lane);
+    }
+    __syncthreads();   // spectrum complete; the raw slot is consumed
+    if (RING > 0 && threadIdx.x == 0 && pair + RING * (int)gridDim.x < npairs)
+      issue(pair + RING * gridDim.x, it % RING);
+
+    // epilogue as in rc_kernel, Z[k] = Xs[k mod zp][k / zp]
+    const int ma = ra / a.n_rx, mb = (ra + 1) / a.n_rx;
+    const float sa = a.scale * (a.wsar ? __ldg(a.wsar + ma) : 1.f);
+    const float sb = a.scale * (a.wsar ? __ldg(a.wsar + mb) : 1.f);
+    float2* pa = a.prof + (size_t)ra * a.n_bins;
+    float2* pb = pa + a.n_bins;
+    for (int i = threadIdx.x; i < a.n_bins; i += WARPS * 32) {
+      const int k = a.k_lo + i;
+      const int kn = (N - k) & (N - 1);
+      const float2 Zk = xs[(k & (zp - 1)) * RS + rpos(k >> lzp)];
+      const float2 Zn = xs[(kn & (zp - 1)) * RS + rpos(kn >> lzp)];
+      const float2 r = __ldg(a.ramp + i);
+      const float2 A = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
+      const float2 B = make_float2(0.5f * (Zk.y + Zn.y), -0.5f * (Zk.x - Zn.x));
+      const float2 Ar = cmul(A, r), Br = cmul(B, r);
+      const bool in_spec = k <= (N >> 1);
+      pa[i] = in_spec ? make_float2(sa * Ar.x, sa * Ar.y) : make_float2(0.f, 0.f);
+      if (has_b) pb[i] = in_spec ? make_float2(sb * Br.x, sb * Br.y) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();   // the spectrum rows are free for the next pair
+  }
+}
+
+constexpr int kRcRing = 4;
+
+template <int L, int WARPS, int RING>
+cudaError_t launch_warp_ring(const RcArgs& a, cudaStream_t s) {
+  auto kern = rc_kernel_warp<L, WARPS, RING>;
+  const size_t smem = (size_t)(a.nfft / L) * RcWarpPlan<L>::RS * sizeof(float2) +
+                      (RING > 0 ? (size_t)RING * (2 * a.ns * sizeof(float) + 8) : 0);
+  static std::atomic<int> configured[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if ((int)smem > configured[dev].load()) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured[dev].store((int)smem);
+  }
+  int resident = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, WARPS * 32, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int npairs = (a.nrows + 1) / 2;
+  const int grid = std::max(1, std::min(npairs, std::max(1, resident) * sms));
+  kern<<<grid, WARPS * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int L, int WARPS>
+cudaError_t launch_warp(const RcArgs& a, cudaStream_t s) {
+  // bulk copies need 16-B aligned rows in device memory
+  cudaPointerAttributes pa;
+  const bool dev_mem = cudaPointerGetAttributes(&pa, a.raw) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+  if (dev_mem && a.ns % 4 == 0 && (reinterpret_cast<uintptr_t>(a.raw) & 15) == 0)
+    return launch_warp_ring<L, WARPS, kRcRing>(a, s);
+  cudaGetLastError();   // clear a failed attribute query
+  return launch_warp_ring<L, WARPS, 0>(a, s);
+}
+
 }  // namespace
+
+// Which kernel transforms this plan's rows: the register path when the nonzero samples fit
+// one L-point transform (L = 256 or 512), else the classic shared-memory FFT.
+// SAR_RC_CLASSIC=1 forces the classic kernel (tests cover both).
+int rc_path(int ns, int nfft, bool allow_env) {
+  const char* e = allow_env ? getenv("SAR_RC_CLASSIC") : nullptr;
+  if (e && e[0] == '1') return 0;
+  if (ns <= 256 && nfft >= 256) return 256;
+  if (ns <= 512 && nfft >= 512) return 512;
+  return 0;
+}
 
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s) {
   constexpr int kBlock = 256;
@@ -165,6 +416,14 @@ cudaError_t launch_rc(const RcArgs& a, cudaStream_t s) {
                                          (16384 + 512 + 1) * (int)sizeof(float2));
     if (e != cudaSuccess) return e;
     configured[dev].store(true);
+  }
+  const int L = rc_path(a.ns, a.nfft);
+  if (L) {
+    const int zp = a.nfft / L;
+    if (L == 256) return zp >= 8 ? launch_warp<256, 8>(a, s) : zp >= 4 ? launch_warp<256, 4>(a, s)
+                                 : zp >= 2 ? launch_warp<256, 2>(a, s) : launch_warp<256, 1>(a, s);
+    return zp >= 8 ? launch_warp<512, 8>(a, s) : zp >= 4 ? launch_warp<512, 4>(a, s)
+                   : zp >= 2 ? launch_warp<512, 2>(a, s) : launch_warp<512, 1>(a, s);
   }
   const int grid = (a.nrows + 1) / 2;
   rc_kernel<kBlock><<<grid, kBlock, smem, s>>>(a);

@@ -31,6 +31,9 @@ struct RcArgs {
   int row0, nrows;         // rows of the chirp shard
   int n_rx, ns, nfft, log2n, k_lo, n_bins;
   float scale;             // 2 / sum(window)
+  // register path (rc_path() = L > 0): plan tables built in fp64
+  const float2* coef;      // [N/L][ns]  w[t] exp(-j 2 pi b t / N): window x stage-0 pre-twiddle
+  const float2* stw;       // stage twiddles: [8][8] W_64^(k r), then [64][R2] W_L^(k r)
 };
 
 // Back-projection kernel arguments (bp_kernel.cu).
@@ -71,6 +74,7 @@ struct BpArgs {
 bool bp_shape_supported(int ncw, int pb);
 size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
+int rc_path(int ns, int nfft, bool allow_env = true);   // 0: classic shared-memory FFT, else the register path's L
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s);
 
 // Doppler-table kernel arguments (doppler_kernel.cu).
@@ -124,6 +128,8 @@ struct sar_plan_s {
   float rc_scale;
   float* d_window = nullptr;
   float2* d_twiddle = nullptr;
+  float2* d_rc_coef = nullptr;   // register-path range-compression tables (rc_kernel.cu)
+  float2* d_rc_stw = nullptr;
   float2* d_ramp = nullptr;
   float2* d_binphase = nullptr;
   // sar_form_image workspace (lazily allocated under ws_mutex)

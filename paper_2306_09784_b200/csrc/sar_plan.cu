@@ -284,6 +284,8 @@ void free_plan(sar_plan_s* p) {
   if (!p) return;
   cudaFree(p->d_window);
   cudaFree(p->d_twiddle);
+  cudaFree(p->d_rc_coef);
+  cudaFree(p->d_rc_stw);
   cudaFree(p->d_ramp);
   cudaFree(p->d_binphase);
 
@@ -448,6 +450,38 @@ static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_
     cyc -= floor(cyc);
     bph[i] = make_float2((float)cos(2.0 * sar::kPi * cyc), (float)sin(2.0 * sar::kPi * cyc));
   }
+  // register-path range compression (rc_kernel.cu): per sub-transform b < N/L the window
+  // times the pre-twiddle exp(-j 2 pi b t / N), and the Stockham stage twiddles W_64^(k r)
+  // (k, r < 8) then W_L^(k r) (k < 64, r < R2 = L/64)
+  const int rcL = sar::rc_path(ns, N, false);
+  std::vector<float2> coef, stw;
+  if (rcL) {
+    const int zp = N / rcL, r2 = rcL / 64;
+    coef.resize((size_t)zp * ns);
+    for (int b = 0; b < zp; ++b)
+      for (int t = 0; t < ns; ++t) {
+        const double a = -2.0 * sar::kPi * (double)(((long long)b * t) % N) / (double)N;
+        const double w = radar->range_window == 1 ? 0.5 - 0.5 * cos(2.0 * sar::kPi * t / (ns - 1)) : 1.0;
+        coef[(size_t)b * ns + t] = make_float2((float)(w * cos(a)), (float)(w * sin(a)));
+      }
+    stw.resize(64 + 64 * r2);
+    for (int k = 0; k < 8; ++k)
+      for (int r = 0; r < 8; ++r) {
+        const double a = -2.0 * sar::kPi * (double)(k * r) / 64.0;
+        stw[k * 8 + r] = make_float2((float)cos(a), (float)sin(a));
+      }
+    for (int k = 0; k < 64; ++k)
+      for (int r = 0; r < r2; ++r) {
+        const double a = -2.0 * sar::kPi * (double)(k * r) / (double)rcL;
+        stw[64 + k * r2 + r] = make_float2((float)cos(a), (float)sin(a));
+      }
+    if ((st = dev_alloc(&p->d_rc_coef, coef.size())) != SAR_OK || (st = dev_alloc(&p->d_rc_stw, stw.size())) != SAR_OK ||
+        (e = cudaMemcpy(p->d_rc_coef, coef.data(), coef.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(p->d_rc_stw, stw.data(), stw.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      free_plan(p);
+      return st != SAR_OK ? st : cuda_fail(e, "cudaMemcpy (range-compression tables)");
+    }
+  }
   if ((st = dev_alloc(&p->d_window, ns)) != SAR_OK || (st = dev_alloc(&p->d_twiddle, tw.size())) != SAR_OK ||
       (st = dev_alloc(&p->d_ramp, ramp.size())) != SAR_OK || (st = dev_alloc(&p->d_binphase, bph.size())) != SAR_OK) {
     free_plan(p);
@@ -494,6 +528,8 @@ sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* 
   a.wsar = w_sar;
   a.window = plan->d_window;
   a.twiddle = plan->d_twiddle;
+  a.coef = plan->d_rc_coef;
+  a.stw = plan->d_rc_stw;
   a.ramp = plan->d_ramp;
   a.prof = reinterpret_cast<float2*>(profiles);
   a.row0 = chirp0 * r.n_rx;

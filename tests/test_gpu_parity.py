@@ -20,9 +20,22 @@ def _raw(scn):
 
 
 # ----------------------------------------------------------------------------- range compression
-@pytest.mark.parametrize("cfg", ["C1", "small_hann", "small_rect_odd", "C2_256"])
-def test_rc_profiles_match_oracle(cuda_lib, cfg):
-    if cfg == "C1":
+@pytest.mark.parametrize("path", ["register", "classic"])
+@pytest.mark.parametrize("cfg", ["C1", "small_hann", "small_rect_odd", "C2_256", "ns500_z1", "ns200_z2",
+                                 "ns300_z16"])
+def test_rc_profiles_match_oracle(cuda_lib, cfg, path, monkeypatch):
+    """Both range-compression kernels (the register path: Zp = N/L warp transforms of length
+    L = 256/512; the classic shared-memory FFT, forced by SAR_RC_CLASSIC=1) on every
+    transform shape class: Z = 1, 2, 4, 8, 16, 32, odd log2 N, ragged Ns, odd row counts."""
+    if path == "classic":
+        monkeypatch.setenv("SAR_RC_CLASSIC", "1")
+    else:
+        monkeypatch.delenv("SAR_RC_CLASSIC", raising=False)
+    if cfg.startswith("ns"):
+        ns, nfft = {"ns500_z1": (500, 512), "ns200_z2": (200, 512), "ns300_z16": (300, 8192)}[cfg]
+        scn = sarsim.small_config(n_chirps=9, ns=128, n_rx=1, seed=7, noise_sigma=0.1)
+        scn.radar = sarsim.Radar(n_samples=ns, fft_len=nfft, range_window=1)
+    elif cfg == "C1":
         scn = sarsim.make_config("C1", wsar="hann")
     elif cfg == "small_hann":
         scn = sarsim.small_config(n_chirps=37, ns=128, n_rx=3, seed=5, noise_sigma=0.1)
