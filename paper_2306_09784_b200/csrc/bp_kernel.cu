@@ -197,7 +197,7 @@ __device__ __forceinline__ f32x2 leg_delta2(const float4 A, const f32x2 UX, cons
 // Shared-memory layout (bytes, 16-B aligned):
 //   [0, 128)                     mbarriers full[kBpMaxStages], empty[kBpMaxStages]
 //   rec   [S][LEGS] x 32 B       monostatic: LEGS = items; bistatic: LEGS = CB + items
-//   kwin  [S][items] int2        {window start bin (crop-relative), profile row offset}
+//   kwin  [S][items] int2        {window start bin (crop-relative), profile row}
 //   win   [S][items][W] x 16 B   pair-format profile windows
 struct Layout {
   int items, legs;
@@ -331,7 +331,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         srec[2 * ri] = leg0;
         srec[2 * ri + 1] = make_float4((float)(kap - k0 - 0.5 - wh), __uint_as_float(off),
                                        NEAR ? (float)(dz * dz) : 0.f, 0.f);
-        skw[e] = make_int2(k0, a.pairs ? (m * a.n_rx + n) : (m * a.n_rx + n) * a.n_bins);
+        skw[e] = make_int2(k0, m * a.n_rx + n);   // profile row (size_t offsets below: rows x n_bins may exceed 2^31)
       }
       __syncwarp();
       if (a.pairs) {
@@ -368,7 +368,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             if (e < items) {
               const int2 kw = skw[e];
               const int k = kw.x + j;
-              if (k >= 0 && k < a.n_bins) x[b] = __ldg(a.prof + kw.y + k);
+              if (k >= 0 && k < a.n_bins) x[b] = __ldg(a.prof + (size_t)kw.y * a.n_bins + k);
             }
           }
 #pragma unroll
