@@ -143,3 +143,18 @@ def test_bp_kernel_sass_uses_bulk_copies_packed_fp32_and_mbarriers():
     assert bp, "bp_kernel_mono not found in libsar.so"
     for mnemonic in ("UBLKCP", "FFMA2", "MUFU.RSQ", "MUFU.SIN", "MUFU.COS", "SYNCS.ARRIVE", "SYNCS.PHASECHK"):
         assert mnemonic in bp, mnemonic
+
+
+def test_rc_register_path_sass_uses_bulk_copy_ring():
+    """The register-path range compression's raw-row ring: 1-D bulk copies (UBLKCP) completing
+    on mbarriers (SYNCS), warp-level exchanges only inside the FFT (one block barrier per
+    row pair before and after the epilogue)."""
+    _build.build()
+    sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    ring = [f for f in funcs if f.startswith("_ZN3sar") and "rc_kernel_warpILi512ELi8ELi4E" in f.split("\n", 1)[0]]
+    assert ring, "rc_kernel_warp<512, 8, 4> not found in libsar.so"
+    body = ring[0]
+    for mnemonic in ("UBLKCP", "SYNCS.PHASECHK", "LDS.64", "STS.64"):
+        assert mnemonic in body, mnemonic
+    assert body.count("BAR.SYNC") <= 3
