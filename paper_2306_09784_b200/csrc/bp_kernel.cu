@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include "ptx_util.h"
@@ -695,10 +696,14 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   int cur_dev = 0;
   if (cudaGetDevice(&cur_dev) != cudaSuccess || cur_dev < 0 || cur_dev >= kMaxDevices) return cudaErrorInvalidDevice;
   if ((int)L.total > configured_bytes[cur_dev].load()) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-    if (e != cudaSuccess) return e;
-    int prev = configured_bytes[cur_dev].load();
-    while ((int)L.total > prev && !configured_bytes[cur_dev].compare_exchange_weak(prev, (int)L.total)) {
+    // only ever raised, under a lock: a concurrent launch of a smaller plan cannot lower the
+    // opt-in below what another thread's launch needs
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)L.total > configured_bytes[cur_dev].load()) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      if (e != cudaSuccess) return e;
+      configured_bytes[cur_dev].store((int)L.total);
     }
   }
   BpArgs b = a;

@@ -364,13 +364,17 @@ cudaError_t launch_warp_ring(const RcArgs& a, cudaStream_t s) {
   auto kern = rc_kernel_warp<L, WARPS, RING>;
   const size_t smem = (size_t)(a.nfft / L) * RcWarpPlan<L>::RS * sizeof(float2) +
                       (RING > 0 ? (size_t)RING * (2 * a.ns * sizeof(float) + 8) : 0);
-  static std::atomic<int> configured[kMaxDevices];
+  // the opt-in is per device: set once to the largest plan this instantiation can see
+  // (N = 16384, Ns = L), so concurrent launches never lower it
+  constexpr int kMaxSmem = (16384 / L) * RcWarpPlan<L>::RS * (int)sizeof(float2) +
+                           (RING > 0 ? RING * (2 * L * (int)sizeof(float) + 8) : 0);
+  static std::atomic<bool> configured[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-  if ((int)smem > configured[dev].load()) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!configured[dev].load()) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return e;
-    configured[dev].store((int)smem);
+    configured[dev].store(true);
   }
   int resident = 0, sms = 148;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, WARPS * 32, smem);
