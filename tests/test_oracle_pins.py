@@ -127,6 +127,26 @@ def test_T3_point_target_C1():
     assert 0.9975 * 64 < abs(p) <= 64.0 + 1e-9
 
 
+def test_T3_bistatic_point_target():
+    """MIMO form of T3 (TX at the pose, 4 RX ahead of it): the image peaks on the target pixel,
+    arg P(p*) = arg a, and |P(p*)| = |a| sum_m sum_n G(a1 (d_tx + d_rx)) with the closed-form
+    interpolation gain.  A bistatic path counted as 2 d_tx or 2 d_rx (the monostatic shortcut)
+    leaves a phase error of 2 pi f0 (d_rx - d_tx)/c per RX -- radians at these offsets."""
+    scn = sarsim.make_config("C1")
+    r = scn.radar
+    scn.rx = sarsim.rx_array(scn.tx, 4, 0.005, r.wavelength_m / 2.0)
+    scn.amps = np.array([0.7 * np.exp(1.1j)])
+    img = _image(scn).reshape(64, 64)
+    assert np.unravel_index(np.argmax(np.abs(img)), img.shape) == (32, 32)
+    p = img[32, 32]
+    assert abs(np.angle(p * np.conj(scn.amps[0]))) < 1e-6
+    a1 = (r.bandwidth_hz / r.chirp_s) * r.fft_len / (C_LIGHT * r.sample_rate_hz)
+    d = np.linalg.norm(scn.tx - scn.targets[0], axis=1)[:, None] + np.linalg.norm(scn.rx - scn.targets[0], axis=2)
+    G = sum(_interp_gain(r, a1 * dm) for dm in d.ravel())
+    assert abs(abs(p) - abs(scn.amps[0]) * G) < 1e-6 * G
+    assert 0.9975 * 0.7 * 64 * 4 < abs(p) <= 0.7 * 64 * 4 + 1e-9
+
+
 def test_T3_argmax_random_single_targets():
     """Matched-filter argmax lands on the scatterer's pixel (SPEC-style property, 12 seeds)."""
     for seed in range(12):
