@@ -63,9 +63,17 @@ constexpr int kBatch = SAR_BP_BATCH;     // producer: profile rows loaded per ba
 #endif
 constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
 #ifndef SAR_BP_MIN_SPLIT
-#define SAR_BP_MIN_SPLIT 512               // chirp split: (chirp, RX) items per chunk at least
+#define SAR_BP_MIN_SPLIT 256               // chirp split: (chirp, RX) items per chunk at least
 #endif
 constexpr long kMinSplitItems = SAR_BP_MIN_SPLIT;
+#ifndef SAR_BP_SPLIT_WAVES
+// chirp split: aim for this many waves of resident CTAs.  Beyond filling the GPU, chirp chunks
+// shorten the tail wave and make the CTAs resident at one time stream fewer distinct pair rows
+// through L2 (chunk-major order); measured (tools/libsweep.sh) 8 -> 32 waves: C3 58.94 -> 58.73 ms,
+// C0 10.08 -> 9.94, C2 24.14 -> 23.83, C6 11.42 -> 11.22, C6p 1.522 -> 1.499 ms
+#define SAR_BP_SPLIT_WAVES 32
+#endif
+constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
 #ifndef SAR_BP_RX_UNROLL
 #define SAR_BP_RX_UNROLL 4                // bistatic RX-loop unroll (C4 1146 -> 1112 ms; 2 is slower)
 #endif
@@ -717,10 +725,13 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
   const long slots = (long)std::max(1, resident) * sms;
   int k = 1;
-  while (ntiles * k < 8 * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems && a.nchirp / (2 * k) >= a.CB)
+  while (ntiles * k < kSplitWaves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
+         a.nchirp / (2 * k) >= a.CB)
     k *= 2;
-  if (a.split_query) {   // planning query: the split a plain launch would use; nothing runs
-    *a.split_query = k;
+  if (a.split_query) {
+    // planning query (sar_form_image), nothing runs: 1 when an unsplit launch fills at least
+    // 8 waves on its own (its epilogue may then store straight to host memory), else the split
+    *a.split_query = ntiles >= 8 * slots ? 1 : k;
     return cudaSuccess;
   }
   if (a.n_peer > 0) k = 1;   // scatter epilogue: stores, no chirp split

@@ -763,7 +763,8 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
                           reinterpret_cast<sar_complex64_t*>(plan->w_prof), stream);
   if (st != SAR_OK) return st;
   // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
-  // under UVA) and the shard fills the GPU without a chirp split (asked of the launcher), every
+  // under UVA) and the shard fills the GPU (>= 8 waves) without a chirp split (asked of the
+  // launcher; the direct-store launch does not split), every
   // finished tile is stored straight into host memory while the other tiles compute; else
   // one device->host copy after the kernel.
   void* mapped = nullptr;
