@@ -18,6 +18,10 @@
 #include "ptx_util.h"
 #include "sar_internal.h"
 
+#ifndef SAR_RC_MINB
+#define SAR_RC_MINB 3
+#endif
+
 namespace sar {
 namespace {
 
@@ -261,7 +265,7 @@ __device__ __forceinline__ void stockham_stage(float2* v, float2* row, const flo
 // the HBM latency of the next ones.  RING = 0 reads the rows with plain loads (rows not 16-B
 // aligned, or raw samples in mapped host memory).
 template <int L, int WARPS, int RING>
-__global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? 3 : 1) rc_kernel_warp(const RcArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_kernel_warp(const RcArgs a) {
   extern __shared__ __align__(16) float2 xs[];   // [zp][RS] | raw ring [RING][2 ns] | mbarriers
   constexpr int E = RcWarpPlan<L>::E, RS = RcWarpPlan<L>::RS;
   const int N = a.nfft;
@@ -357,7 +361,10 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? 3 : 1) rc_kernel_warp
   }
 }
 
-constexpr int kRcRing = 4;
+#ifndef SAR_RC_RING
+#define SAR_RC_RING 4
+#endif
+constexpr int kRcRing = SAR_RC_RING;
 
 template <int L, int WARPS, int RING>
 cudaError_t launch_warp_ring(const RcArgs& a, cudaStream_t s) {
