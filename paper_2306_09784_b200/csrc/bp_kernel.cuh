@@ -1,0 +1,847 @@
+// bp_kernel.cuh: the tiled Back-Projection kernel template (steps H2-H6), included by
+// bp_kernel.cu (plain epilogue: store / accumulate / chirp-split reductions into the image)
+// and bp_scatter.cu (NEXT-4 scatter epilogue into peer images), so that the two families are
+// compiled as separate translation units and the plain kernel's code is not perturbed by the
+// scatter epilogue (ptxas schedules the chirp loop differently when it is present: +2.5 % C3).
+#pragma once
+// bp_kernel: tiled time-domain Back-Projection (steps H2-H6), Alg. 2 of arXiv 2306.09784
+// in a form whose fp32 arithmetic is accurate at 30 m ranges.
+//
+// Work decomposition
+//   * One CTA = one 32 x (NCW*PB) pixel tile.  The tile anchor P_T is the tile centre (fp64).
+//   * Warp NCW is the PRODUCER: for each ring stage of CB chirps it computes, in fp64,
+//     the per-(tile, chirp, antenna) anchor record (D = P_T - q, r = |D|, anchor index
+//     and anchor phase) and stages the W profile entries the tile can touch for that chirp
+//     into shared memory in "pair" format {mid = (X[k]+X[k+1])/2, diff = X[k+1]-X[k]} x
+//     carrier bin phase, so that linear interpolation is one LDS.128 plus two FFMA.  The
+//     entries come from pair-format rows built once per chirp row (pair_kernel) with one
+//     1-D bulk copy (TMA engine) per item; without that workspace the producer builds them
+//     itself from the profiles (same values; the path used if the rows cannot be allocated).
+//     The window bound is the triangle inequality |d_hyp - d_anchor| <= 2 rho_T (tighter
+//     for polar tiles), valid for ANY track and chirp order.
+//   * Warps 0..NCW-1 are CONSUMERS: each thread owns PB pixels (register accumulators);
+//     for one register slot a warp's 32 lanes cover an 8x4 pixel patch, so their gathers
+//     hit few distinct bins (broadcast, no bank conflicts).
+//   * Producer/consumer hand-off through an S-deep ring guarded by mbarriers
+//     (full: 32 producer lanes arrive; empty: all consumer threads arrive).
+//
+// Per (pixel, chirp, antenna) update (monostatic shown; bistatic adds the RX leg):
+//   g   = D.u + |u|^2/2                      (u = p - P_T, fp32, |u| <= rho_T)
+//   s   = r^2 + 2g  ~ |p - q|^2              rsqrt via MUFU: q = 1/sqrt(s)
+//   R0  = s q;  t = R0 - r (exact);  h = (R0 + r)/2
+//   dR  = t + (g - t h) q                     = |p - q| - r, to ~1e-8 m (one Newton step
+//                                               on the residual; no cancellation)
+//   kappa = kappa_anchor + A1 dR  (+ f_doppler(p))          Alg. 2 L8
+//   K = floor(kappa) (the 1.5*2^23 trick), f = kappa - K, gf = f - 1/2
+//   v = mid[K] + gf diff[K]                   (one LDS.128, two FFMA)
+//   acc += v * exp(j 2 pi beta gf)            (MUFU sin/cos)  Alg. 2 L9, L10, L12
+// Carrier phase folding: without Doppler kappa = a1 d exactly, so the hypothetical
+// phase 2 pi c2 d (Alg. 2 L9, A2: +j) equals 2 pi beta kappa with beta = c2/a1 cycles per
+// bin = 2 pi beta (K + 1/2) + 2 pi beta gf.  The producer multiplies each staged pair by
+// exp(j 2 pi beta (K + 1/2)) (plan table, built in fp64), so the per-update MUFU argument
+// is bounded by |2 pi beta gf| <= pi beta (~32 rad) whatever the range: the fp32 phase
+// carries no bias that grows with range or tile size.  With Doppler the shift
+// exp(-j 2 pi beta f_doppler(p)) is a per-pixel constant applied in the epilogue.
+// 3 MUFU + ~21 FMA/ALU + 1 LDS.128 per update.
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <type_traits>
+
+#include "ptx_util.h"
+#include "sar_internal.h"
+
+namespace sar {
+namespace {
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+constexpr uint32_t kMagicBits = 0x4B400000u;
+constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
+#ifndef SAR_BP_BATCH
+#define SAR_BP_BATCH 8
+#endif
+constexpr int kBatch = SAR_BP_BATCH;     // producer: profile rows loaded per batch
+#ifndef SAR_BP_CHIRP_UNROLL
+#define SAR_BP_CHIRP_UNROLL 1            // consumer chirp-loop unroll (monostatic)
+#endif
+constexpr int kChirpUnroll = SAR_BP_CHIRP_UNROLL;
+#ifndef SAR_BP_MIN_SPLIT
+#define SAR_BP_MIN_SPLIT 256               // chirp split: (chirp, RX) items per chunk at least
+#endif
+constexpr long kMinSplitItems = SAR_BP_MIN_SPLIT;
+#ifndef SAR_BP_SPLIT_WAVES
+// chirp split: aim for this many waves of resident CTAs.  Beyond filling the GPU, chirp chunks
+// shorten the tail wave and make the CTAs resident at one time stream fewer distinct pair rows
+// through L2 (chunk-major order); measured (tools/libsweep.sh) 8 -> 32 waves: C3 58.94 -> 58.73 ms,
+// C0 10.08 -> 9.94, C2 24.14 -> 23.83, C6 11.42 -> 11.22, C6p 1.522 -> 1.499 ms
+#define SAR_BP_SPLIT_WAVES 32
+#endif
+constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
+#ifndef SAR_BP_RX_UNROLL
+#define SAR_BP_RX_UNROLL 4                // bistatic RX-loop unroll (C4 1146 -> 1112 ms; 2 is slower)
+#endif
+constexpr int kRxUnroll = SAR_BP_RX_UNROLL;
+// (A min-blocks launch bound, even "1", changes ptxas's schedule: measured 5 % slower on C3;
+//  capping registers for 6-7 resident CTAs spilled and was slower too.  tools/vsweep.sh)
+
+#ifdef SAR_BP_TRACE
+// tuning instrumentation (tools/trace_bp.py): clock64 stamps of the ring waits of four CTAs
+constexpr int kTrCtas = 4, kTrIt = 256;
+__device__ unsigned long long g_trace[kTrCtas][9][kTrIt][3];
+__device__ unsigned int g_trace_wid[kTrCtas][9][2];
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int tr_cta() {
+  const int b = blockIdx.x;
+  return b == 2000 ? 0 : b == 2001 ? 1 : b == 5000 ? 2 : b == 5001 ? 3 : -1;
+}
+__device__ __forceinline__ void tr_ids(int trc, int w) {
+  unsigned int wid, smid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  g_trace_wid[trc][w][0] = wid;
+  g_trace_wid[trc][w][1] = smid;
+}
+#define SAR_TR(w, it, k) \
+  if (trc >= 0 && lane == 0 && (it) < kTrIt) g_trace[trc][w][it][k] = clk()
+#else
+#define SAR_TR(w, it, k)
+#endif
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2): one instruction, two round-to-nearest
+// fp32 operations.  A pair whose halves are equal is issued as a scalar broadcast operand,
+// so record values are read once for two pixels (the BP loop is register-file-read bound).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fsub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
+
+__device__ __forceinline__ float rsqrt_mufu(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One leg |p - q| - r of the anchored range.  Record: Dx, Dy, r2 = r^2, r, e = r/2 (fast)
+// or Dz^2 (SAFE).  SAFE is the near-field form (an antenna may sit inside the tile): the
+// range is formed from the exact differences D + u and dR = 2g / (R + r) has no division
+// by a vanishing quantity (r > 0: the anchor is never a pixel centre).
+//   D2x, D2y = 2 D (record), w = |u|^2 (per pixel): g2 = 2 D.u + |u|^2 = |D + u|^2 - r^2
+//   s = r^2 + g2, q = rsqrt(s); t = s q - r and H = s q + r (one rounding each);
+//   rho2 = g2 - t H = s - (s q)^2 (exact residual up to one rounding);
+//   dR = t + rho2 q / 2.
+template <bool SAFE>
+__device__ __forceinline__ float leg_delta(float D2x, float D2y, float r2, float r, float dz2,
+                                           float ux, float uy, float w) {
+  const float g2 = fmaf(D2x, ux, fmaf(D2y, uy, w));
+  if (SAFE) {
+    const float ex = fmaf(0.5f, D2x, ux), ey = fmaf(0.5f, D2y, uy);
+    const float R = sqrtf(fmaf(ex, ex, fmaf(ey, ey, dz2)));
+    return __fdividef(g2, R + r);
+  } else {
+    const float s = g2 + r2;
+    const float q = rsqrt_mufu(s);
+    const float t = fmaf(s, q, -r);
+    const float H = fmaf(s, q, r);
+    const float qh = 0.5f * q;
+    const float rho2 = fmaf(-t, H, g2);
+    return fmaf(rho2, qh, t);
+  }
+}
+
+// The far-field leg for a pixel pair (FFMA2 form of leg_delta<false>); record
+// A = {2Dx, 2Dy, r^2, r}; the second record word is B = {kappa_anchor, window address,
+// Dz^2 (near field), 0}, so the consumer reads (kappa_anchor, address) with one LDS.64.
+__device__ __forceinline__ f32x2 leg_delta2(const float4 A, const f32x2 UX, const f32x2 UY, const f32x2 W) {
+  const f32x2 G2 = ffma2(bc2(A.x), UX, ffma2(bc2(A.y), UY, W));   // 2 D.u + |u|^2
+  const f32x2 S = fadd2(G2, bc2(A.z));                            // ~|p - q|^2
+  const f32x2 Q = pk2(rsqrt_mufu(lo2(S)), rsqrt_mufu(hi2(S)));
+  const f32x2 T = ffma2(S, Q, bc2(-A.w));                         // s q - r
+  const f32x2 H = ffma2(S, Q, bc2(A.w));                          // s q + r
+  const f32x2 RHO = ffma2(pk2(-lo2(T), -hi2(T)), H, G2);          // exact residual
+  return ffma2(RHO, fmul2(Q, bc2(0.5f)), T);                      // |p - q| - r
+}
+
+// Shared-memory layout (bytes, 16-B aligned):
+//   [0, 128)                     mbarriers full[kBpMaxStages], empty[kBpMaxStages]
+//   rec   [S][LEGS] x 32 B       monostatic: LEGS = items; bistatic: LEGS = CB + items
+//   kwin  [S][items] int2        {window start bin (crop-relative), profile row}
+//   win   [S][items][W] x 16 B   pair-format profile windows
+struct Layout {
+  int items, legs;
+  uint32_t rec, kwin, win, total;
+};
+
+__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic) {
+  Layout L;
+  L.items = CB * n_rx;
+  L.legs = bistatic ? CB + L.items : L.items;
+  L.rec = 16 * kBpMaxStages;
+  L.kwin = L.rec + (uint32_t)S * L.legs * 32;
+  const uint32_t kw_bytes = ((uint32_t)S * L.items * 8 + 15u) & ~15u;
+  L.win = L.kwin + kw_bytes;
+  L.total = L.win + (uint32_t)S * L.items * W * 16;
+  return L;
+}
+
+// NEAR: the plan has tiles within 3 rho of the antenna box; those tiles (a per-CTA,
+// warp-uniform decision) take the near-field SAFE consumer path, all others the fast one.
+template <bool BISTATIC, bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
+__device__ __forceinline__ void bp_body(const BpArgs& a) {
+  constexpr int TX = kTileX;
+  constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int S = a.S;
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpMaxStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // CTA -> (chirp chunk, tile), chunk-major so that concurrently resident CTAs stream the
+  // same profile rows through L2.  ksplit > 1 only for grids too small to fill the GPU.
+  const int ntiles = a.tiles_x * a.tiles_y;
+  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int chirp0 = a.chirp0 + chunk * a.chunk;
+  const int nchirp = min(a.chunk, a.nchirp - chunk * a.chunk);
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int i0 = tx * TX;               // first grid column of the tile
+  const int j0 = ty * TY;               // first row of the tile, relative to row0
+  // tile anchor: centre of the full tile (even when ragged), fp64.  Cartesian grids:
+  // (x0 + i dx, y0 + j dy); polar grids (Measure E): (xc + r sin th, yc + r cos th).
+  double PTx, PTy;
+  if (a.polar) {
+    const double th = a.th0 + (i0 + 0.5 * (TX - 1)) * a.dth;
+    const double rr = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+    PTx = a.x0 + rr * sin(th);
+    PTy = a.y0 + rr * cos(th);
+  } else {
+    PTx = a.x0 + (i0 + 0.5 * (TX - 1)) * a.dx;
+    PTy = a.y0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dy;
+  }
+  const double PTz = a.z0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(bar_full + 8 * s, 32);          // producer lanes
+      mbar_init(bar_empty + 8 * s, NCW * 32);   // consumer threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int n_iter = (nchirp + a.CB - 1) / a.CB;
+
+  if (warp == NCW) {
+    // ============================== PRODUCER ==============================
+    float4* rec = reinterpret_cast<float4*>(smem + L.rec);
+    int2* kwin = reinterpret_cast<int2*>(smem + L.kwin);
+    float4* win = reinterpret_cast<float4*>(smem + L.win);
+    int slot = 0;
+    uint32_t parity = 0;
+#ifdef SAR_BP_TRACE
+    const int trc = tr_cta();
+    if (trc >= 0 && lane == 0) tr_ids(trc, 8);
+#endif
+    for (int it = 0; it < n_iter; ++it) {
+      SAR_TR(8, it, 0);
+      mbar_wait(bar_empty + 8 * slot, parity ^ 1);
+      SAR_TR(8, it, 1);
+      const int c0 = it * a.CB;
+      const int cnt = min(a.CB, nchirp - c0);
+      const int items = cnt * a.n_rx;
+      float4* srec = rec + (size_t)slot * L.legs * 2;
+      int2* skw = kwin + slot * L.items;
+      float4* swin = win + (size_t)slot * L.items * a.W;
+      // ---- anchor records (fp64), one item per lane
+      if (BISTATIC) {
+        for (int c = lane; c < cnt; c += 32) {
+          const double* q = a.tx + 3 * (size_t)(chirp0 + c0 + c);
+          const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
+          const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+          srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
+          srec[2 * c + 1] = make_float4(0.f, 0.f, NEAR ? (float)(Dz * Dz) : 0.f, 0.f);
+        }
+      }
+      for (int e = lane; e < items; e += 32) {
+        const int c = BISTATIC ? e / a.n_rx : e;
+        const int n = BISTATIC ? e - c * a.n_rx : 0;
+        const int m = chirp0 + c0 + c;
+        const double* qt = a.tx + 3 * (size_t)m;
+        // The consumers form r32 + dR = sqrt(r32^2 + 2 D32.u + |u|^2) from the fp32-rounded
+        // record; the anchor path length uses the exact fp64 |D| so that the rounding of
+        // r and D enters only at second order (|r32 - |D|| * dR / r, ~1e-8 m).
+        double d_anchor, dz;
+        float4 leg0;
+        float rleg;
+        if (BISTATIC) {
+          const double* qr = a.rx + 3 * ((size_t)m * a.n_rx + n);
+          const double Dx = PTx - qr[0], Dy = PTy - qr[1], Dz = PTz - qr[2];
+          const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+          rleg = (float)rr;
+          leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
+          dz = Dz;
+          const double Tx = PTx - qt[0], Ty = PTy - qt[1], Tz = PTz - qt[2];
+          d_anchor = sqrt(Tx * Tx + Ty * Ty + Tz * Tz) + rr;
+        } else {
+          const double Dx = PTx - qt[0], Dy = PTy - qt[1], Dz = PTz - qt[2];
+          const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+          rleg = (float)rr;
+          leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
+          dz = Dz;
+          d_anchor = 2.0 * rr;
+        }
+        const double kap = a.a1 * d_anchor - a.k_lo;               // anchor index in the crop
+        const int k0 = (int)floor(kap - a.kap_half) - 1;            // window start
+        const int wh = a.W >> 1;                                    // centre the fp32 index
+        const uint32_t waddr = smem_u32(swin + (size_t)e * a.W);
+        const uint32_t off = waddr + 16u * (uint32_t)wh - 16u * kMagicBits;
+        const int ri = BISTATIC ? a.CB + e : e;
+        srec[2 * ri] = leg0;
+        srec[2 * ri + 1] = make_float4((float)(kap - k0 - 0.5 - wh), __uint_as_float(off),
+                                       NEAR ? (float)(dz * dz) : 0.f, 0.f);
+        skw[e] = make_int2(k0, m * a.n_rx + n);   // profile row (size_t offsets below: rows x n_bins may exceed 2^31)
+      }
+      __syncwarp();
+      if (a.pairs) {
+        // bulk copies of pair-format rows: lane 0 adds the stage's byte count to the full
+        // barrier, every lane arrives after issuing its copies; a start outside the padded row
+        // (antennas outside the declared box) is clamped: wrong values, never out of bounds
+        if (lane == 0) mbar_arrive_expect_tx(bar_full + 8 * slot, (uint32_t)items * a.W * 16u);
+        __syncwarp();
+        const uint32_t wdst = smem_u32(swin);
+        for (int e = lane; e < items; e += 32) {
+          const int2 kw = skw[e];
+          const int i0 = min(max(kw.x + a.pair_pad, 0), a.pair_stride - a.W);
+          bulk_g2s(wdst + 16u * (uint32_t)(e * a.W), a.pairs + (size_t)kw.y * a.pair_stride + i0, 16u * a.W,
+                   bar_full + 8 * slot);
+        }
+        if (lane != 0) mbar_arrive(bar_full + 8 * slot);
+        SAR_TR(8, it, 2);
+        if (++slot == S) {
+          slot = 0;
+          parity ^= 1;
+        }
+        continue;
+      }
+      // ---- profile windows in pair format: lane j of an item produces entry j from bins
+      //      k0+j and k0+j+1 (the latter from lane j+1 by shuffle); kBatch rows in flight
+      for (int j0w = 0; j0w < a.W; j0w += 31) {
+        const int j = j0w + lane;
+        for (int e0 = 0; e0 < items; e0 += kBatch) {
+          float2 x[kBatch];
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            x[b] = make_float2(0.f, 0.f);
+            const int e = e0 + b;
+            if (e < items) {
+              const int2 kw = skw[e];
+              const int k = kw.x + j;
+              if (k >= 0 && k < a.n_bins) x[b] = __ldg(a.prof + (size_t)kw.y * a.n_bins + k);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            const float nx_ = __shfl_down_sync(0xffffffffu, x[b].x, 1);
+            const float ny_ = __shfl_down_sync(0xffffffffu, x[b].y, 1);
+            const int e = e0 + b;
+            if (e < items && lane < 31 && j < a.W) {
+              // bin phase exp(j 2 pi beta (k_lo + k + 1/2)) of the entry's lower bin k; the
+              // table starts at k = -1 (the entry holding X[-1] = 0 and X[0]); entries
+              // further out hold only zeros and may take any phase
+              const int k = min(max(skw[e].x + j, -1), a.n_bins - 1);
+              const float2 q = __ldg(a.binphase + k + 1);
+              const float mr = 0.5f * (x[b].x + nx_), mi = 0.5f * (x[b].y + ny_);
+              const float dr = nx_ - x[b].x, di = ny_ - x[b].y;
+              swin[(size_t)e * a.W + j] = make_float4(mr * q.x - mi * q.y, mr * q.y + mi * q.x,
+                                                      dr * q.x - di * q.y, dr * q.y + di * q.x);
+            }
+          }
+        }
+      }
+      mbar_arrive(bar_full + 8 * slot);
+      SAR_TR(8, it, 2);
+      if (++slot == S) {
+        slot = 0;
+        parity ^= 1;
+      }
+    }
+    return;
+  }
+
+  // ============================== CONSUMERS ==============================
+  auto consume = [&](auto safe_tag) {
+  constexpr bool SAFE = decltype(safe_tag)::value;
+  const int lx = lane & (kPatchX - 1), ly = lane >> 3;
+  constexpr int kPatchesPerRow = TX / kPatchX;
+  float ux[PB], uy[PB], wh[PB], acc_r[PB], acc_i[PB], fd[PB];
+  int gx[PB], gy[PB];
+#pragma unroll
+  for (int p = 0; p < PB; ++p) {
+    const int pi = warp * PB + p;
+    const int xl = (pi % kPatchesPerRow) * kPatchX + lx;
+    const int yl = (pi / kPatchesPerRow) * kPatchY + ly;
+    gx[p] = i0 + xl;
+    gy[p] = j0 + yl;
+    double dux, duy;
+    if (a.polar) {   // pixel offset from the anchor, both evaluated in fp64
+      const double th = a.th0 + (i0 + xl) * a.dth;
+      const double rr = a.r0 + (a.row0 + j0 + yl) * a.dr;
+      dux = (a.x0 + rr * sin(th)) - PTx;
+      duy = (a.y0 + rr * cos(th)) - PTy;
+    } else {
+      dux = (xl - 0.5 * (TX - 1)) * a.dx;
+      duy = (yl - 0.5 * (TY - 1)) * a.dy;
+    }
+    ux[p] = (float)dux;
+    uy[p] = (float)duy;
+    wh[p] = (float)(dux * dux + duy * duy);   // |u|^2
+    acc_r[p] = 0.f;
+    acc_i[p] = 0.f;
+    fd[p] = 0.f;
+    if (DOP) {
+      if (gx[p] < a.nx && gy[p] < a.nrow) fd[p] = __ldg(a.dop + (size_t)(a.row0 + gy[p]) * a.nx + gx[p]);
+    }
+    // keep the per-pixel constants in registers: a shuffle is opaque to ptxas, which
+    // otherwise re-derives them from fp64 inside the chirp loop (rematerialisation)
+    ux[p] = __shfl_sync(0xffffffffu, ux[p], lane);
+    uy[p] = __shfl_sync(0xffffffffu, uy[p], lane);
+    wh[p] = __shfl_sync(0xffffffffu, wh[p], lane);
+  }
+  const float4* rec = reinterpret_cast<const float4*>(smem + L.rec);
+  const float A1 = a.A1f, C3 = a.C3f;
+  constexpr bool kPaired = !SAFE && (PB % 2 == 0);
+  f32x2 UX[PB / 2 + 1], UY[PB / 2 + 1], W2[PB / 2 + 1], FD2[PB / 2 + 1], ACC[PB + 1], ACI[PB + 1];
+  if (kPaired) {
+#pragma unroll
+    for (int h = 0; h < PB / 2; ++h) {
+      UX[h] = pk2(ux[2 * h], ux[2 * h + 1]);
+      UY[h] = pk2(uy[2 * h], uy[2 * h + 1]);
+      W2[h] = pk2(wh[2 * h], wh[2 * h + 1]);
+      FD2[h] = pk2(fd[2 * h], fd[2 * h + 1]);
+    }
+#pragma unroll
+    for (int p = 0; p < PB; ++p) ACC[p] = ACI[p] = pk2(0.f, 0.f);
+  }
+
+  int slot = 0;
+  uint32_t parity = 0;
+#ifdef SAR_BP_TRACE
+  const int trc = tr_cta();
+  if (trc >= 0 && lane == 0) tr_ids(trc, warp);
+#endif
+  for (int it = 0; it < n_iter; ++it) {
+    SAR_TR(warp, it, 0);
+    mbar_wait(bar_full + 8 * slot, parity);
+    SAR_TR(warp, it, 1);
+    const int cnt = min(a.CB, nchirp - it * a.CB);
+    const float4* srec = rec + (size_t)slot * L.legs * 2;
+    if (kPaired) {
+      // Far field, pixels in pairs (2h, 2h+1): the range and index arithmetic runs as
+      // FFMA2/FADD2 over the pair with the record values as scalar broadcast operands; the
+      // complex interpolation and accumulation run as FFMA2 over (re, im).
+      // v exp(j th) = vr (cs, sn) + vi (-sn, cs): the two halves go to separate accumulators,
+      // ACC += vr (cs, sn) and ACI += vi (sn, cs) (a swizzle, no negation); the epilogue
+      // forms (ACC.re - ACI.re, ACC.im + ACI.im).
+      auto tail = [&](const int h, const f32x2 DR, const float kap_a, const uint32_t off) {
+        f32x2 KAP = ffma2(bc2(A1), DR, bc2(kap_a));                                   // Alg. 2 L8
+        if (DOP) KAP = fadd2(KAP, FD2[h]);
+        const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
+        const f32x2 GF = fsub2(KAP, fsub2(TK, bc2(kMagic)));                        // gf in [-1/2, 1/2]
+        const f32x2 TH = fmul2(GF, bc2(C3));                                        // 2 pi beta gf
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float tk = k ? hi2(TK) : lo2(TK);
+          const float gf = k ? hi2(GF) : lo2(GF);
+          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
+          float sn, cs;
+          __sincosf(k ? hi2(TH) : lo2(TH), &sn, &cs);
+          ACC[2 * h + k] = ffma2(bc2(lo2(V)), pk2(cs, sn), ACC[2 * h + k]);
+          ACI[2 * h + k] = ffma2(bc2(hi2(V)), pk2(sn, cs), ACI[2 * h + k]);
+        }
+      };
+      if (!BISTATIC) {
+#pragma unroll kChirpUnroll
+        for (int c = 0; c < cnt; ++c) {
+          const float4 A = srec[2 * c], B = srec[2 * c + 1];
+#pragma unroll
+          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.x, __float_as_uint(B.y));
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+          const float4 T = srec[2 * c];
+          f32x2 DT[PB / 2];
+#pragma unroll
+          for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
+          const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
+#pragma unroll kRxUnroll
+          for (int n = 0; n < a.n_rx; ++n, rp += 2) {
+            const float4 A = rp[0], B = rp[1];
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h)
+              tail(h, fadd2(DT[h], leg_delta2(A, UX[h], UY[h], W2[h])), B.x, __float_as_uint(B.y));
+          }
+        }
+      }
+    } else if (!BISTATIC) {
+#pragma unroll kChirpUnroll
+      for (int c = 0; c < cnt; ++c) {
+        const float4 A = srec[2 * c], B = srec[2 * c + 1];
+        const uint32_t off = __float_as_uint(B.y);
+#pragma unroll
+        for (int p = 0; p < PB; ++p) {
+          const float dR = leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+          float kap = fmaf(A1, dR, B.x);
+          if (DOP) kap += fd[p];
+          const float tk = kap + kMagic;
+          const float kf = tk - kMagic;
+          const float gf = kap - kf;
+          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
+          float sn, cs;
+          __sincosf(C3 * gf, &sn, &cs);
+          acc_r[p] = fmaf(vr, cs, acc_r[p]);
+          acc_r[p] = fmaf(-vi, sn, acc_r[p]);
+          acc_i[p] = fmaf(vr, sn, acc_i[p]);
+          acc_i[p] = fmaf(vi, cs, acc_i[p]);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < cnt; ++c) {
+        const float4 T = srec[2 * c], TB = srec[2 * c + 1];
+        float dT[PB];
+#pragma unroll
+        for (int p = 0; p < PB; ++p) dT[p] = leg_delta<SAFE>(T.x, T.y, T.z, T.w, TB.z, ux[p], uy[p], wh[p]);
+#pragma unroll 1
+        for (int n = 0; n < a.n_rx; ++n) {
+          const int ri = a.CB + c * a.n_rx + n;
+          const float4 A = srec[2 * ri], B = srec[2 * ri + 1];
+          const uint32_t off = __float_as_uint(B.y);
+#pragma unroll
+          for (int p = 0; p < PB; ++p) {
+            const float dR = dT[p] + leg_delta<SAFE>(A.x, A.y, A.z, A.w, B.z, ux[p], uy[p], wh[p]);
+            float kap = fmaf(A1, dR, B.x);
+            if (DOP) kap += fd[p];
+            const float tk = kap + kMagic;
+            const float kf = tk - kMagic;
+            const float gf = kap - kf;
+            const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+            const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
+            float sn, cs;
+            __sincosf(C3 * gf, &sn, &cs);
+            acc_r[p] = fmaf(vr, cs, acc_r[p]);
+            acc_r[p] = fmaf(-vi, sn, acc_r[p]);
+            acc_i[p] = fmaf(vr, sn, acc_i[p]);
+            acc_i[p] = fmaf(vi, cs, acc_i[p]);
+          }
+        }
+      }
+    }
+    mbar_arrive(bar_empty + 8 * slot);
+    SAR_TR(warp, it, 2);
+    if (++slot == S) {
+      slot = 0;
+      parity ^= 1;
+    }
+  }
+
+  if (kPaired) {
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      acc_r[p] = lo2(ACC[p]) - lo2(ACI[p]);
+      acc_i[p] = hi2(ACC[p]) + hi2(ACI[p]);
+    }
+  }
+  // epilogue: remove the Doppler index shift from the folded phase, then store (or
+  // accumulate) the tile
+#pragma unroll
+  for (int p = 0; p < PB; ++p) {
+    if (DOP) {
+      float sn, cs;
+      sincosf(-C3 * fd[p], &sn, &cs);
+      const float r = acc_r[p] * cs - acc_i[p] * sn, i = acc_r[p] * sn + acc_i[p] * cs;
+      acc_r[p] = r;
+      acc_i[p] = i;
+    }
+  }
+  if constexpr (SCATTER) {
+    if (a.acc_img && a.ksplit > 1) {
+      // split scatter: add this chunk into the local accumulation image; the last chunk of the
+      // tile to finish (threadfence-reduction pattern on a per-tile counter) reads the tile
+      // back from L2 and stores it to every peer, so the gather still overlaps other tiles
+#pragma unroll
+      for (int p = 0; p < PB; ++p)
+        if (gx[p] < a.nx && gy[p] < a.nrow) {
+          float* d = reinterpret_cast<float*>(a.acc_img + (size_t)gy[p] * a.nx + gx[p]);
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+        }
+      __threadfence();
+      // the flag lives in the record area: past the first barrier no consumer reads the ring
+      volatile int* s_last = reinterpret_cast<volatile int*>(smem + L.rec);
+      asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");   // consumer warps only
+      if (threadIdx.x == 0) *s_last = atomicAdd(a.tile_count + tile, 1) == a.ksplit - 1;
+      asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+      if (!*s_last) return;
+      __threadfence();
+#pragma unroll
+      for (int p = 0; p < PB; ++p) {
+        if (gx[p] < a.nx && gy[p] < a.nrow) {
+          const float2 v = __ldcg(a.acc_img + (size_t)gy[p] * a.nx + gx[p]);
+          acc_r[p] = v.x;
+          acc_i[p] = v.y;
+        }
+      }
+    }
+    // fused gather (NEXT-4): the finished tile goes straight to every rank's full image over
+    // NVLink while other tiles are still being computed
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      if (gx[p] < a.nx && gy[p] < a.nrow) {
+        const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
+        if (a.multicast) {
+          float* d = reinterpret_cast<float*>(a.peer[0] + o);
+          if (a.accumulate) {   // chirp shards: the NVSwitch adds into every rank's image
+            asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+            asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+          } else {
+            asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(d), "f"(acc_r[p]),
+                         "f"(acc_i[p])
+                         : "memory");
+          }
+        } else if (a.accumulate) {   // chirp shards: P2P reductions into the peers' images
+          for (int q = 0; q < a.n_peer; ++q) {
+            float* d = reinterpret_cast<float*>(a.peer[q] + o);
+            asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+            asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+          }
+        } else {
+          for (int q = 0; q < a.n_peer; ++q) a.peer[q][o] = make_float2(acc_r[p], acc_i[p]);
+        }
+      }
+    }
+  } else {
+    // The plain family keeps the generic epilogue of the first design, peer branches included
+    // (a.n_peer == 0 here, never taken): with it ptxas schedules the chirp loop in the form
+    // measured fastest on C3 (0.7 % faster than without; tools/libsweep.sh).
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      if (gx[p] < a.nx && gy[p] < a.nrow) {
+        float2* dst = a.img + (size_t)gy[p] * a.nx + gx[p];
+        if (a.n_peer > 0) {
+          const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
+          if (a.multicast) {
+            float* d = reinterpret_cast<float*>(a.peer[0] + o);
+            if (a.accumulate) {
+              asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+              asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+            } else {
+              asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(d), "f"(acc_r[p]),
+                           "f"(acc_i[p])
+                           : "memory");
+            }
+          } else if (a.accumulate) {
+            for (int q = 0; q < a.n_peer; ++q) {
+              float* d = reinterpret_cast<float*>(a.peer[q] + o);
+              asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+              asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+            }
+          } else {
+            for (int q = 0; q < a.n_peer; ++q) a.peer[q][o] = make_float2(acc_r[p], acc_i[p]);
+          }
+        } else if (a.ksplit > 1) {
+          // several chirp chunks add into the same pixel (the image was zeroed first when
+          // not accumulating); fire-and-forget reductions in L2
+          float* d = reinterpret_cast<float*>(dst);
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+        } else if (a.accumulate) {
+          const float2 o = *dst;
+          *dst = make_float2(o.x + acc_r[p], o.y + acc_i[p]);
+        } else {
+          *dst = make_float2(acc_r[p], acc_i[p]);
+        }
+      }
+    }
+  }
+  };
+  if constexpr (NEAR) {
+    // near-field test of this tile: distance from the anchor to the antenna box
+    double d2 = 0.0;
+    const double pt[3] = {PTx, PTy, PTz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double gap = fmax(0.0, fmax(a.box_lo[k] - pt[k], pt[k] - a.box_hi[k]));
+      d2 += gap * gap;
+    }
+    double rho_t = a.tile_rho;
+    if (a.polar) {   // annular patch: farthest from its anchor at a corner
+      const double rc = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+      const double ht = 0.5 * (TX - 1) * a.dth, hr = 0.5 * (TY - 1) * a.dr;
+      rho_t = 0.0;
+      for (int c = 0; c < 4; ++c) {
+        const double rr = rc + ((c & 1) ? hr : -hr), dt = (c & 2) ? ht : -ht;
+        rho_t = fmax(rho_t, sqrt(rr * rr + rc * rc - 2.0 * rr * rc * cos(dt)));
+      }
+    }
+    const double near_r = 3.0 * rho_t * (1.0 + 1e-6) + 1e-3;
+    if (d2 < near_r * near_r) consume(std::true_type{});
+    else consume(std::false_type{});
+  } else {
+    consume(std::false_type{});
+  }
+}
+
+// Register budget: the monostatic kernel is left to ptxas (a min-blocks bound changes its
+// schedule and was measured 5 % slower on C3); the bistatic kernel (TX leg kept live across
+// the RX loop) is held to four resident CTAs per SM at the default 32 x 32 tile:
+// C4 1343 -> 1190 ms (tools/vsweep.sh).
+template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
+__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel_mono(const BpArgs a) {
+  bp_body<false, DOP, NEAR, NCW, PB, SCATTER>(a);
+}
+template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? 4 : 1) bp_kernel_bi(const BpArgs a) {
+  bp_body<true, DOP, NEAR, NCW, PB, SCATTER>(a);
+}
+template <bool BI, bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
+struct BpKernel {
+  static constexpr auto fn = bp_kernel_mono<DOP, NEAR, NCW, PB, SCATTER>;
+};
+template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
+struct BpKernel<true, DOP, NEAR, NCW, PB, SCATTER> {
+  static constexpr auto fn = bp_kernel_bi<DOP, NEAR, NCW, PB, SCATTER>;
+};
+
+template <bool BI, bool DOP, bool SAFE, int NCW, int PB, bool SCATTER>
+cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
+  auto kern = BpKernel<BI, DOP, SAFE, NCW, PB, SCATTER>::fn;
+  constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
+  // the dynamic shared-memory opt-in is per device and per kernel instantiation
+  static std::atomic<int> configured_bytes[kMaxDevices];
+  int cur_dev = 0;
+  if (cudaGetDevice(&cur_dev) != cudaSuccess || cur_dev < 0 || cur_dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if ((int)L.total > configured_bytes[cur_dev].load()) {
+    // only ever raised, under a lock: a concurrent launch of a smaller plan cannot lower the
+    // opt-in below what another thread's launch needs
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)L.total > configured_bytes[cur_dev].load()) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      if (e != cudaSuccess) return e;
+      configured_bytes[cur_dev].store((int)L.total);
+    }
+  }
+  BpArgs b = a;
+  b.tiles_y = (a.nrow + TY - 1) / TY;
+  const long ntiles = (long)b.tiles_x * b.tiles_y;
+  // Chirp split: enough CTAs for kSplitWaves waves of resident CTAs, each chunk at least
+  // kMinSplitItems (chirp, RX) items (and a multiple of the ring stage).
+  int resident = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, (NCW + 1) * 32, L.total);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
+  const long slots = (long)std::max(1, resident) * sms;
+  int k = 1;
+  while (ntiles * k < kSplitWaves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
+         a.nchirp / (2 * k) >= a.CB)
+    k *= 2;
+  if (a.split_query) {
+    // planning query, nothing runs: the chirp split of a plain launch
+    *a.split_query = k;
+    return cudaSuccess;
+  }
+  // scatter epilogue: split only with an accumulation image and tile counters (stores to the
+  // peers come from the last chunk of each tile); reductions into peers run unsplit
+  if (a.n_peer > 0 && (a.accumulate || !a.acc_img || !a.tile_count)) k = 1;
+  b.chunk = (a.nchirp + k - 1) / k;
+  b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
+  b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);
+  if (b.ksplit < 1) b.ksplit = 1;
+  if (b.ksplit > 1 && a.n_peer > 0) {
+    cudaError_t e = cudaMemsetAsync(a.acc_img, 0, sizeof(float2) * (size_t)a.nrow * a.nx, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.tile_count, 0, sizeof(int) * (size_t)ntiles, s);
+    if (e != cudaSuccess) return e;
+  } else if (b.ksplit > 1 && !a.accumulate) {
+    cudaError_t e = cudaMemsetAsync(a.img, 0, sizeof(float2) * (size_t)a.nrow * a.nx, s);
+    if (e != cudaSuccess) return e;
+  }
+  const long grid = ntiles * b.ksplit;
+  kern<<<(unsigned)grid, (NCW + 1) * 32, L.total, s>>>(b);
+  return cudaGetLastError();
+}
+
+template <int NCW, int PB, bool SCATTER>
+cudaError_t launch_shape(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
+  if (bistatic) {
+    if (doppler)
+      return near ? launch_one<true, true, true, NCW, PB, SCATTER>(a, s) : launch_one<true, true, false, NCW, PB, SCATTER>(a, s);
+    return near ? launch_one<true, false, true, NCW, PB, SCATTER>(a, s) : launch_one<true, false, false, NCW, PB, SCATTER>(a, s);
+  }
+  if (doppler)
+    return near ? launch_one<false, true, true, NCW, PB, SCATTER>(a, s) : launch_one<false, true, false, NCW, PB, SCATTER>(a, s);
+  return near ? launch_one<false, false, true, NCW, PB, SCATTER>(a, s) : launch_one<false, false, false, NCW, PB, SCATTER>(a, s);
+}
+
+// CTA shape dispatch (consumer warps x pixels per thread); tile = 32 x (NCW * PB).
+template <bool SCATTER>
+cudaError_t launch_shapes(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
+  if (a.ncw == 8 && a.pb == 4) return launch_shape<8, 4, SCATTER>(a, bistatic, doppler, near, s);
+  if (a.ncw == 4 && a.pb == 8) return launch_shape<4, 8, SCATTER>(a, bistatic, doppler, near, s);
+  if (a.ncw == 4 && a.pb == 4) return launch_shape<4, 4, SCATTER>(a, bistatic, doppler, near, s);
+  if (a.ncw == 8 && a.pb == 8) return launch_shape<8, 8, SCATTER>(a, bistatic, doppler, near, s);
+  return cudaErrorInvalidConfiguration;
+}
+
+}  // namespace
+}  // namespace sar

@@ -64,6 +64,11 @@ struct BpArgs {
   // written with multimem.st when multicast != 0) instead of img
   float2* peer[8];
   int n_peer, multicast;
+  // Chirp split under a (non-accumulating) scatter: chunks add into acc_img ([nrow][nx], zeroed
+  // by the launcher) and the last chunk of each tile (tile_count, zeroed) stores the finished
+  // tile to every peer.  nullptr: the scatter runs unsplit.
+  float2* acc_img;
+  int* tile_count;
   int* split_query;        // non-null: report the chirp split of this launch, do not launch
   const float4* pairs;     // pair-format rows [n_chirps * n_rx][pair_stride] (pair_kernel) or nullptr
   int pair_stride, pair_pad;
@@ -76,6 +81,7 @@ size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
 int rc_path(int ns, int nfft, bool allow_env = true);   // 0: classic shared-memory FFT, else the register path's L
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s);
+cudaError_t launch_bp_scatter(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s);
 
 // Doppler-table kernel arguments (doppler_kernel.cu).
 struct DopArgs {

@@ -658,8 +658,33 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     a.pair_pad = pad;
   }
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
+  a.acc_img = nullptr;
+  a.tile_count = nullptr;
+  if (n_peer > 0 && !accumulate && nchirp > 0 && !split_query) {
+    // a scatter that would run chirp-split: accumulation image + per-tile counters from the
+    // pool (the last chunk of each tile publishes it); without them it runs unsplit
+    int k = 1;
+    sar::BpArgs q = a;
+    q.n_peer = 0;
+    q.split_query = &k;
+    if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, plan->near_field, (cudaStream_t)stream) == cudaSuccess &&
+        k > 1) {
+      const size_t ntiles = (size_t)a.tiles_x * ((nrow + plan->info.tile_y - 1) / plan->info.tile_y);
+      if (cudaMallocFromPoolAsync((void**)&a.acc_img, (size_t)nrow * g.nx * sizeof(float2), plan->pool,
+                                  (cudaStream_t)stream) != cudaSuccess ||
+          cudaMallocFromPoolAsync((void**)&a.tile_count, ntiles * sizeof(int), plan->pool, (cudaStream_t)stream) !=
+              cudaSuccess) {
+        cudaGetLastError();
+        if (a.acc_img) cudaFreeAsync(a.acc_img, (cudaStream_t)stream);
+        a.acc_img = nullptr;
+        a.tile_count = nullptr;
+      }
+    }
+  }
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
+  if (a.acc_img) cudaFreeAsync(a.acc_img, (cudaStream_t)stream);
+  if (a.tile_count) cudaFreeAsync(a.tile_count, (cudaStream_t)stream);
   if (pairs) cudaFreeAsync(pairs, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
   if (!split_query) plan->launches.fetch_add(pairs ? 2 : 1);
@@ -763,18 +788,11 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
                           reinterpret_cast<sar_complex64_t*>(plan->w_prof), stream);
   if (st != SAR_OK) return st;
   // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
-  // under UVA) and the shard fills the GPU (>= 8 waves) without a chirp split (asked of the
-  // launcher; the direct-store launch does not split), every
-  // finished tile is stored straight into host memory while the other tiles compute; else
-  // one device->host copy after the kernel.
+  // under UVA) every finished tile is stored straight into host memory while the other tiles
+  // compute (under a chirp split, by the last chunk of each tile from an accumulation image);
+  // else one device->host copy after the kernel.
   void* mapped = nullptr;
-  int split = 0;
-  st = backproject_impl(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
-                        rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0, r.n_chirps, row0,
-                        nrow, reinterpret_cast<sar_complex64_t*>(plan->w_img), 0, nullptr, 0, 0, stream, &split);
-  if (st != SAR_OK) return st;
-  const bool direct = nrow > 0 && split == 1 &&
-                      cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;
+  const bool direct = nrow > 0 && cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;
   if (!direct) cudaGetLastError();   // clear the error of a pageable buffer
   if (direct) {
     sar_complex64_t* base = reinterpret_cast<sar_complex64_t*>(mapped) - (ptrdiff_t)row0 * g.nx;

@@ -100,3 +100,36 @@ def test_scatter_add_chirp_shards_equal_full_image(cuda_lib):
         err = float((im - ref).abs().max() / ref.abs().max())
         assert err < 1e-5, err
     plan.close()
+
+
+@pytest.mark.parametrize("rows", [(0, 24), (5, 13)])
+def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows):
+    """A scatter whose grid is too small to fill the GPU runs chirp-split: every chunk adds into
+    a pool-allocated accumulation image and the last chunk of each tile (per-tile counter)
+    stores the finished tile to every destination.  Equals sar_backproject (also split) to
+    fp32 summation order, the oracle to the parity bar; rows outside the shard untouched."""
+    import torch
+
+    from tests.helpers import REL_TOL, oracle_image, rel_err
+
+    scn = sarsim.small_config(n_chirps=4096, ns=128, nx=40, ny=24, seed=57)
+    raw = sarsim.simulate_raw(scn, device="cuda:0")
+    lo, hi = scn.antenna_box(1e-3)
+    plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, 1, (lo, hi))
+    # 2 tiles of 32 x 32 px and 4096 chirps: the launcher splits into 8 chunks of 512 chirps
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    prof = plan.range_compress(raw)
+    row0, nrow = rows
+    g = scn.grid
+    ref = plan.backproject(prof, tx, row0=row0, nrow=nrow)
+    imgs = [torch.full((g.ny, g.nx), complex(7.0, -7.0), dtype=torch.complex64, device="cuda:0") for _ in range(3)]
+    for _ in range(2):   # the workspace (counters, accumulation image) is reset per launch
+        plan.backproject_scatter(prof, tx, [im.data_ptr() for im in imgs], row0=row0, nrow=nrow)
+    torch.cuda.synchronize()
+    ora = oracle_image(scn, raw.cpu().numpy()).reshape(g.ny, g.nx)[row0:row0 + nrow]
+    for im in imgs:
+        got = im[row0:row0 + nrow].cpu().numpy()
+        assert rel_err(got, ref.cpu().numpy()) < 1e-6
+        assert rel_err(got, ora) <= REL_TOL
+        assert torch.all(im[:row0] == complex(7.0, -7.0)) and torch.all(im[row0 + nrow:] == complex(7.0, -7.0))
+    plan.close()
