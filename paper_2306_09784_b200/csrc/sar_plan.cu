@@ -660,12 +660,15 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
   a.acc_img = nullptr;
   a.tile_count = nullptr;
-  if (n_peer > 0 && !accumulate && nchirp > 0 && !split_query) {
+  static const bool scatter_nosplit = [] {   // tuning switch: scatters always unsplit
+    const char* e = getenv("SAR_BP_SCATTER_NOSPLIT");
+    return e && e[0] == '1';
+  }();
+  if (n_peer > 0 && !accumulate && nchirp > 0 && !split_query && !scatter_nosplit) {
     // a scatter that would run chirp-split: accumulation image + per-tile counters from the
     // pool (the last chunk of each tile publishes it); without them it runs unsplit
     int k = 1;
-    sar::BpArgs q = a;
-    q.n_peer = 0;
+    sar::BpArgs q = a;   // the launcher's split of this scatter (its unsplit policy included)
     q.split_query = &k;
     if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, plan->near_field, (cudaStream_t)stream) == cudaSuccess &&
         k > 1) {
@@ -789,7 +792,8 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   if (st != SAR_OK) return st;
   // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
   // under UVA) every finished tile is stored straight into host memory while the other tiles
-  // compute (under a chirp split, by the last chunk of each tile from an accumulation image);
+  // compute (unsplit when that fills 6 waves, else under a chirp split by the last chunk of
+  // each tile from an accumulation image);
   // else one device->host copy after the kernel.
   void* mapped = nullptr;
   const bool direct = nrow > 0 && cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;

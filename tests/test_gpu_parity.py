@@ -328,9 +328,9 @@ def test_form_image_direct_host_stores_equal_device_path(cuda_lib, cfg, rows):
     """Shards that fill the GPU without a chirp split and a pinned host image take the fused
     readback (the BP epilogue stores into mapped host memory; pinned raw samples are read by
     the range compression in place); smaller shards and pageable images take the copy path.
-    The direct path equals the unsplit device launch (the scatter epilogue into a device image)
-    bit for bit; the copy path equals sar_backproject bit for bit; the two differ only by the
-    fp32 order of the chirp-chunk sums sar_backproject may use (32-wave split)."""
+    The copy path equals sar_backproject bit for bit; the direct path (unsplit when that fills
+    8 waves) and the scatter into a device image differ from it only by the fp32 order of the
+    chirp-chunk sums (32-wave split)."""
     import torch
 
     scn = sarsim.make_config(cfg, n_chirps=512)
@@ -347,7 +347,7 @@ def test_form_image_direct_host_stores_equal_device_path(cuda_lib, cfg, rows):
     raw_h, tx_h = raw.cpu().pin_memory(), torch.as_tensor(scn.tx).pin_memory()
     pinned = torch.full((nrow, scn.grid.nx), complex(5.0, 5.0), dtype=torch.complex64).pin_memory()
     out = plan.form_image(raw_h, tx_h, row0=row0, nrow=nrow, out_h=pinned)
-    assert torch.equal(out, unsplit) or torch.equal(out, ref)
+    assert rel_err(out.numpy(), ref.numpy()) < 1e-6
     assert rel_err(unsplit.numpy(), ref.numpy()) < 1e-6
     pageable = torch.empty((nrow, scn.grid.nx), dtype=torch.complex64)
     out2 = plan.form_image(raw_h, tx_h, row0=row0, nrow=nrow, out_h=pageable)
