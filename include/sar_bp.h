@@ -196,7 +196,11 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
  *                               multimem.st / multimem.red reach every rank's image at once
  * With symmetric memory the images are the P2P-mapped buffers of every rank (one NVLink
  * store or reduction per peer).  Rows outside [row0, row0 + nrow) are not touched; the caller
- * orders the ranks (e.g. a symmetric-memory barrier) before reading.  No chirp split.
+ * orders the ranks (e.g. a symmetric-memory barrier) before reading.  A store scatter whose
+ * shard cannot fill 6 waves of the GPU unsplit runs chirp-split: the chunks add into a
+ * stream-ordered accumulation image from the plan's pool and the last chunk of each tile
+ * stores the finished tile (SAR_ERR_NO_MEMORY never results: without the workspace it runs
+ * unsplit).  SAR_SCATTER_ADD runs unsplit.
  *   images  host array of n_images device pointers (may be peer or multicast addresses) */
 #define SAR_SCATTER_MULTICAST 1
 #define SAR_SCATTER_ADD 2
@@ -210,10 +214,11 @@ sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* pro
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a
  * plan-owned device workspace, runs sar_range_compress over all chirps and
  * sar_backproject over all chirps for grid rows [row0, row0 + nrow), and returns
- * those image rows, all on `stream`.  When image_host is pinned (device-mapped) and
- * the shard fills the GPU without a chirp split, the BP epilogue stores each finished
- * tile straight into image_host (readback overlapped with the compute); otherwise one
- * copy follows the kernel.  A pinned raw_host is read by the range compression directly.
+ * those image rows, all on `stream`.  When image_host is pinned (device-mapped), the
+ * BP epilogue stores each finished tile straight into image_host (readback overlapped
+ * with the compute; under a chirp split the last chunk of each tile stores it);
+ * otherwise one copy follows the kernel.  A pinned raw_host is read by the range
+ * compression directly.
  *   raw_host [n_chirps][n_rx][n_samples] float; w_sar_host [n_chirps] float or NULL;
  *   tx_host [n_chirps][3] double; rx_host [n_chirps][n_rx][3] double or NULL;
  *   doppler_host [ny][nx] float or NULL; image_host [nrow][nx] complex (written).
