@@ -197,7 +197,7 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
  * With symmetric memory the images are the P2P-mapped buffers of every rank (one NVLink
  * store or reduction per peer).  Rows outside [row0, row0 + nrow) are not touched; the caller
  * orders the ranks (e.g. a symmetric-memory barrier) before reading.  A store scatter whose
- * shard cannot fill 6 waves of the GPU unsplit runs chirp-split: the chunks add into a
+ * shard cannot fill 7 waves of the GPU unsplit runs chirp-split: the chunks add into a
  * stream-ordered accumulation image from the plan's pool and the last chunk of each tile
  * stores the finished tile (SAR_ERR_NO_MEMORY never results: without the workspace it runs
  * unsplit).  SAR_SCATTER_ADD runs unsplit.

@@ -796,9 +796,10 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   while (ntiles * k < kSplitWaves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
          a.nchirp / (2 * k) >= a.CB)
     k *= 2;
-  // scatters: unsplit when that already fills 6 waves (measured on C3 row shards: unsplit
-  // +1.0 % over the plain split launch at 7.5 waves, +5.9 % at 3.7; split publish +2.4 %)
-  if (a.n_peer > 0 && ntiles >= 6 * slots) k = 1;
+  // scatters: unsplit when that already fills 7 waves.  Cost over the plain split launch,
+  // measured: unsplit +1.0 % at 7.5 waves (C3 rows / 2), +4 % at 6.0 (C2 to a host image),
+  // +5.9 % at 3.7 (C3 rows / 4); the split publish costs +2.4 %
+  if (a.n_peer > 0 && ntiles >= 7 * slots) k = 1;
   if (a.split_query) {
     // planning query, nothing runs: the chirp split of a plain launch
     *a.split_query = k;
