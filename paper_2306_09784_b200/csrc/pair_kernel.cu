@@ -1,5 +1,6 @@
 // pair_kernel: profiles -> pair-format rows for the BP producer's bulk copies.
-// Entry i of a row holds, for the lower bin k = i - pad,
+// Entry i of a row holds, for the lower crop bin k = k0 + i - pad (k0 > 0: a row shard's
+// own crop),
 //   {mid = (X[k] + X[k+1]) / 2, diff = X[k+1] - X[k]} * exp(j 2 pi beta (k_lo + k + 1/2))
 // with X = 0 outside the crop (A8): the same values the BP producer otherwise builds per
 // (tile, chirp) window, built once per chirp row instead.  HBM-bound: 8 n_bins B read,
@@ -16,7 +17,7 @@ __global__ void pair_kernel(const PairArgs a) {
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < n; idx += (long)gridDim.x * blockDim.x) {
     const long row = idx / a.stride;
     const int i = (int)(idx - row * a.stride);
-    const int k = i - a.pad;
+    const int k = a.k0 + i - a.pad;
     const float2* x = a.prof + (size_t)(a.row0 + row) * a.n_bins;
     const float2 x0 = (k >= 0 && k < a.n_bins) ? __ldg(x + k) : make_float2(0.f, 0.f);
     const float2 x1 = (k + 1 >= 0 && k + 1 < a.n_bins) ? __ldg(x + k + 1) : make_float2(0.f, 0.f);

@@ -71,7 +71,7 @@ struct BpArgs {
   int* tile_count;
   int* split_query;        // non-null: report the chirp split of this launch, do not launch
   const float4* pairs;     // pair-format rows [n_chirps * n_rx][pair_stride] (pair_kernel) or nullptr
-  int pair_stride, pair_pad;
+  int pair_stride, pair_pad;   // entry of crop bin k: k + pair_pad (pad minus the rows' first bin)
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
   float C3f;               // 2 pi beta: carrier phase (rad) per range bin
 };
@@ -114,6 +114,7 @@ struct PairArgs {
   const float2* binphase;  // [n_bins + 1], from k = -1
   float4* out;             // [rows][stride]
   int row0, rows, n_bins, stride, pad;
+  int k0;                  // first crop bin the rows cover (a row shard's own crop)
 };
 cudaError_t launch_pairs(const PairArgs& a, cudaStream_t s);
 

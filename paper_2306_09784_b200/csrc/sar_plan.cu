@@ -82,6 +82,52 @@ sar_status_t polar_box(const sar_polar_grid_t* pg, double lo[3], double hi[3], s
   return SAR_OK;
 }
 
+// Crop of the one-sided spectrum a (sub-)grid needs: every two-way path from the declared
+// antenna box to the grid's box (and, for a polar grid, through its centre) lies in
+// [d_min, d_max]; bins [k_lo, k_hi] with interpolation margin, even row length.
+sar_status_t crop_bins(const sar_radar_params_t* r, const sar_grid_t* g, const sar_box_t* b,
+                       const sar_polar_grid_t* pg, double a1, double* d_min, double* d_max, long* k_lo,
+                       long* k_hi) {
+  double glo[3] = {g->x0, g->y0, g->z0};
+  double ghi[3] = {g->x0 + (g->nx - 1) * g->dx, g->y0 + (g->ny - 1) * g->dy, g->z0};
+  if (pg) {
+    sar_grid_t tmp;
+    sar_status_t st = polar_box(pg, glo, ghi, &tmp);
+    if (st != SAR_OK) return st;
+  }
+  double dist_min, dist_max;
+  box_distance(glo, ghi, b->lo, b->hi, &dist_min, &dist_max);
+  if (pg) {
+    // an annular sector is poorly described by its bounding box: also bound each leg
+    // through the polar centre c, r - |q - c| <= |p - q| <= r + |q - c|
+    double sc = 0.0;
+    for (int cx = 0; cx < 2; ++cx)
+      for (int cy = 0; cy < 2; ++cy)
+        for (int cz = 0; cz < 2; ++cz) {
+          const double ex = (cx ? b->hi[0] : b->lo[0]) - pg->xc, ey = (cy ? b->hi[1] : b->lo[1]) - pg->yc,
+                       ez = (cz ? b->hi[2] : b->lo[2]) - pg->zc;
+          sc = std::max(sc, sqrt(ex * ex + ey * ey + ez * ez));
+        }
+    const double r1 = pg->r0 + (pg->n_r - 1) * pg->dr;
+    dist_min = std::max(dist_min, pg->r0 - sc);
+    dist_max = std::min(dist_max, r1 + sc);
+  }
+  *d_min = 2.0 * dist_min;  // each leg lies in [dist_min, dist_max]
+  *d_max = 2.0 * dist_max;
+  const double dop = r->doppler_max_bins;
+  const long half = r->fft_len / 2;
+  long lo_ = (long)floor(a1 * *d_min - dop) - 2;
+  long hi_ = (long)floor(a1 * *d_max + dop) + 3;
+  lo_ = std::max(0L, std::min(lo_, half));
+  hi_ = std::max(lo_, std::min(hi_, half));
+  // even row length (16-B aligned rows); the extra bin may be N/2 + 1, which the range
+  // compression writes as 0 (A8)
+  if ((hi_ - lo_ + 1) & 1) ++hi_;
+  *k_lo = lo_;
+  *k_hi = hi_;
+  return SAR_OK;
+}
+
 // Host-side plan maths shared by sar_plan_geometry and sar_plan_create (pg: polar grid or
 // nullptr; g then is the Cartesian stand-in from polar_box).
 sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_box_t* b,
@@ -116,41 +162,11 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   I.a1_bins_per_m = I.chirp_rate_hz_per_s * N / (sar::kLightSpeed * r->sample_rate_hz);
   I.c2_cycles_per_m = r->f0_hz / sar::kLightSpeed;                         // f0 / c (A3)
 
-  double glo[3] = {g->x0, g->y0, g->z0};
-  double ghi[3] = {g->x0 + (g->nx - 1) * g->dx, g->y0 + (g->ny - 1) * g->dy, g->z0};
-  if (pg) {
-    sar_grid_t tmp;
-    sar_status_t st = polar_box(pg, glo, ghi, &tmp);
-    if (st != SAR_OK) return st;
-  }
-  double dist_min, dist_max;
-  box_distance(glo, ghi, b->lo, b->hi, &dist_min, &dist_max);
-  if (pg) {
-    // an annular sector is poorly described by its bounding box: also bound each leg
-    // through the polar centre c, r - |q - c| <= |p - q| <= r + |q - c|
-    double sc = 0.0;
-    for (int cx = 0; cx < 2; ++cx)
-      for (int cy = 0; cy < 2; ++cy)
-        for (int cz = 0; cz < 2; ++cz) {
-          const double ex = (cx ? b->hi[0] : b->lo[0]) - pg->xc, ey = (cy ? b->hi[1] : b->lo[1]) - pg->yc,
-                       ez = (cz ? b->hi[2] : b->lo[2]) - pg->zc;
-          sc = std::max(sc, sqrt(ex * ex + ey * ey + ez * ez));
-        }
-    const double r1 = pg->r0 + (pg->n_r - 1) * pg->dr;
-    dist_min = std::max(dist_min, pg->r0 - sc);
-    dist_max = std::min(dist_max, r1 + sc);
-  }
-  I.d_min_m = 2.0 * dist_min;  // each leg lies in [dist_min, dist_max]
-  I.d_max_m = 2.0 * dist_max;
+  long k_lo, k_hi;
+  sar_status_t cst = crop_bins(r, g, b, pg, I.a1_bins_per_m, &I.d_min_m, &I.d_max_m, &k_lo, &k_hi);
+  if (cst != SAR_OK) return cst;
   const double dop = r->doppler_max_bins;
-  const long half = r->fft_len / 2;
-  long k_lo = (long)floor(I.a1_bins_per_m * I.d_min_m - dop) - 2;
-  long k_hi = (long)floor(I.a1_bins_per_m * I.d_max_m + dop) + 3;
-  k_lo = std::max(0L, std::min(k_lo, half));
-  k_hi = std::max(k_lo, std::min(k_hi, half));
-  // even row length (16-B aligned rows); the extra bin may be N/2 + 1, which the range
-  // compression writes as 0 (A8)
-  if ((k_hi - k_lo + 1) & 1) ++k_hi;
+  const double dist_min = 0.5 * I.d_min_m;   // one leg
   I.k_lo = (int32_t)k_lo;
   I.n_bins = (int32_t)(k_hi - k_lo + 1);
 
@@ -623,11 +639,34 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     const char* e = getenv("SAR_BP_NO_PAIRS");
     return e && e[0] == '1';
   }();
+  // Pair rows cover the bins of this call's rows only (a row shard's own crop, same margins
+  // as the plan's; windows of tiles reaching past the shard fall in the zero-extended pad)
+  int kb0 = 0, kbn = plan->info.n_bins;
+  if (row0 != 0 || nrow != g.ny) {
+    sar_grid_t sg = g;
+    sar_polar_grid_t spg = plan->pgrid;
+    if (plan->polar) {
+      spg.r0 = plan->pgrid.r0 + row0 * plan->pgrid.dr;
+      spg.n_r = nrow;
+    } else {
+      sg.y0 = g.y0 + row0 * g.dy;
+    }
+    sg.ny = nrow;
+    double dmin, dmax;
+    long lo, hi;
+    if (crop_bins(&r, &sg, &plan->box, plan->polar ? &spg : nullptr, plan->info.a1_bins_per_m, &dmin, &dmax, &lo,
+                  &hi) == SAR_OK) {
+      const long b0 = std::max(0L, std::min(lo - plan->info.k_lo, (long)plan->info.n_bins));
+      const long b1 = std::max(b0, std::min(hi - plan->info.k_lo + 1, (long)plan->info.n_bins));
+      kb0 = (int)b0;
+      kbn = (int)(b1 - b0);
+    }
+  }
   if (nchirp > 0 && !split_query && !no_pairs) {
     // Pair-format rows of this call's chirps (pair_kernel, HBM-bound), in a stream-ordered
     // allocation from the plan's pool so that calls on different streams stay independent;
     // the BP producer then only issues one bulk copy per (tile, chirp, RX) window.
-    const int pad = plan->info.window_bins + 2, stride = plan->info.n_bins + 2 * pad;
+    const int pad = plan->info.window_bins + 2, stride = kbn + 2 * pad;
     const size_t rows = (size_t)nchirp * r.n_rx;
     cudaError_t pe = cudaMallocFromPoolAsync((void**)&pairs, rows * stride * sizeof(float4), plan->pool,
                                              (cudaStream_t)stream);
@@ -637,7 +676,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     }
   }
   if (pairs) {
-    const int pad = plan->info.window_bins + 2, stride = plan->info.n_bins + 2 * pad;
+    const int pad = plan->info.window_bins + 2, stride = kbn + 2 * pad;
     const size_t rows = (size_t)nchirp * r.n_rx;
     sar::PairArgs pa;
     pa.prof = a.prof + (size_t)chirp0 * r.n_rx * plan->info.n_bins;
@@ -648,6 +687,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     pa.n_bins = plan->info.n_bins;
     pa.stride = stride;
     pa.pad = pad;
+    pa.k0 = kb0;
     cudaError_t pe = sar::launch_pairs(pa, (cudaStream_t)stream);
     if (pe != cudaSuccess) {
       cudaFreeAsync(pairs, (cudaStream_t)stream);
@@ -655,7 +695,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     }
     a.pairs = pairs - (size_t)chirp0 * r.n_rx * stride;   // indexed by absolute (chirp, RX) row
     a.pair_stride = stride;
-    a.pair_pad = pad;
+    a.pair_pad = pad - kb0;
   }
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
   a.acc_img = nullptr;
