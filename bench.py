@@ -312,15 +312,18 @@ def run_ours(args):
     launches = plan.launches - l0
     gather_check = None
     if fused is not None:
-        # outside the timed region: the fused image must equal the NCCL gather of the rows
+        # outside the timed region: the fused image must equal the NCCL gather of the rows up
+        # to the fp32 order of chirp-chunk sums (both launches may be chirp-split; their L2
+        # reductions land in any order)
         plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
         from paper_2306_09784_b200.dist import gather_rows
 
         ref = gather_rows(local_img, g.ny)
         torch.cuda.synchronize()
-        gather_check = bool(torch.equal(ref, fused.image))
-        if not gather_check:
-            print("bench: fused gather differs from the NCCL gather", file=sys.stderr)
+        rel = float((ref - fused.image).abs().max() / ref.abs().max().clamp_min(1e-30))
+        gather_check = {"equal": bool(torch.equal(ref, fused.image)), "max_rel_diff": rel, "ok": rel <= 1e-5}
+        if not gather_check["ok"]:
+            print(f"bench: fused gather differs from the NCCL gather (max rel {rel:.2e})", file=sys.stderr)
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms, sum(bp_ms)], dtype=torch.float64, device=dev)
