@@ -204,6 +204,11 @@ def test_doppler_full_chain_matches_oracle(cuda_lib):
     ref = oracle_image(scn, raw.cpu().numpy(), doppler=oracle.doppler_table(r, grid.pixels(), q_ref, v_avg))
     assert rel_err(got, ref) <= REL_TOL
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    # a row shard: its pair rows cover only the shard's own crop (Doppler margin included)
+    part = gpu_image(scn, raw, doppler=dop, dop_max=dmax, row0=70, nrow=50).cpu().numpy()
+    ref2 = ref.reshape(grid.ny, grid.nx)[70:120]
+    assert np.abs(part - ref2).max() <= REL_TOL * np.abs(ref).max()
+    assert rel_err(part, ref2) <= 2 * REL_TOL
 
 
 def test_near_field_pixel_on_antenna(cuda_lib):

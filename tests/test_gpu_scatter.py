@@ -102,8 +102,8 @@ def test_scatter_add_chirp_shards_equal_full_image(cuda_lib):
     plan.close()
 
 
-@pytest.mark.parametrize("rows", [(0, 24), (5, 13)])
-def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows):
+@pytest.mark.parametrize("rows,n_rx", [((0, 24), 1), ((5, 13), 1), ((3, 17), 3)])
+def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows, n_rx):
     """A scatter whose grid is too small to fill the GPU runs chirp-split: every chunk adds into
     a pool-allocated accumulation image and the last chunk of each tile (per-tile counter)
     stores the finished tile to every destination.  Equals sar_backproject (also split) to
@@ -112,19 +112,20 @@ def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows):
 
     from tests.helpers import REL_TOL, oracle_image, rel_err
 
-    scn = sarsim.small_config(n_chirps=4096, ns=128, nx=40, ny=24, seed=57)
+    scn = sarsim.small_config(n_chirps=4096 // n_rx, ns=128, nx=40, ny=24, seed=57, n_rx=n_rx)
     raw = sarsim.simulate_raw(scn, device="cuda:0")
     lo, hi = scn.antenna_box(1e-3)
-    plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, 1, (lo, hi))
+    plan = cuda_lib.Plan(scn.radar, scn.grid, scn.n_chirps, n_rx, (lo, hi))
+    rx = None if n_rx == 1 else torch.as_tensor(scn.rx, device="cuda:0").contiguous()
     # 2 tiles of 32 x 32 px and 4096 chirps: the launcher splits into 8 chunks of 512 chirps
     tx = torch.as_tensor(scn.tx, device="cuda:0")
     prof = plan.range_compress(raw)
     row0, nrow = rows
     g = scn.grid
-    ref = plan.backproject(prof, tx, row0=row0, nrow=nrow)
+    ref = plan.backproject(prof, tx, rx, row0=row0, nrow=nrow)
     imgs = [torch.full((g.ny, g.nx), complex(7.0, -7.0), dtype=torch.complex64, device="cuda:0") for _ in range(3)]
     for _ in range(2):   # the workspace (counters, accumulation image) is reset per launch
-        plan.backproject_scatter(prof, tx, [im.data_ptr() for im in imgs], row0=row0, nrow=nrow)
+        plan.backproject_scatter(prof, tx, [im.data_ptr() for im in imgs], rx, row0=row0, nrow=nrow)
     torch.cuda.synchronize()
     ora = oracle_image(scn, raw.cpu().numpy()).reshape(g.ny, g.nx)[row0:row0 + nrow]
     for im in imgs:
