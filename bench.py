@@ -278,10 +278,16 @@ def run_ours(args):
             plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
             ev[2].record(stream)
         if world > 1 and fused is None:
-            dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1),
-                                        torch.view_as_real(local_img).view(-1))
+            if g.ny % world == 0:
+                dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1),
+                                            torch.view_as_real(local_img).view(-1))
+            else:   # ragged row blocks: padded gather (dist.gather_rows)
+                from paper_2306_09784_b200.dist import gather_rows
+
+                full_img.copy_(gather_rows(local_img, g.ny))
         if polar:
-            sar.polar_to_cartesian(g, full_img, cart, out=cart_img, stream=stream)
+            sar.polar_to_cartesian(g, fused.image if fused is not None else full_img, cart, out=cart_img,
+                                   stream=stream)
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     for _ in range(args.warmup):
