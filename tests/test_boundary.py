@@ -5,6 +5,7 @@ import math
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -158,3 +159,13 @@ def test_rc_register_path_sass_uses_bulk_copy_ring():
     for mnemonic in ("UBLKCP", "SYNCS.PHASECHK", "LDS.64", "STS.64"):
         assert mnemonic in body, mnemonic
     assert body.count("BAR.SYNC") <= 3
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: with libsar.so absent the binding raises on first use."""
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2306_09784_b200 import sar\n"
+            "try:\n    sar.load()\nexcept ImportError as e:\n    print('raised', e)\n") % ROOT
+    env = dict(os.environ, SAR_LIB=str(tmp_path / "libsar.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and "raised" in out.stdout and "missing" in out.stdout
