@@ -177,7 +177,11 @@ sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* 
  *                         doppler_max_bins >= max |doppler_bins| in the plan
  *   image     dev complex [nrow][nx]: row r holds grid row row0 + r
  *   accumulate 0: image = P;  1: image += P (chirp sharding, NCCL reduce)
- * nrow == 0 is a no-op; nchirp == 0 writes zeros (accumulate = 0) or nothing. */
+ * nrow == 0 is a no-op; nchirp == 0 writes zeros (accumulate = 0) or nothing.
+ * Pixels are computed in absolute grid tiles (see sar_backproject_tiles), so any row shard
+ * reproduces the unsharded image's pixels.  A launch too small to fill the GPU splits its
+ * chirps into chunks whose partial images (stream-ordered workspace from the plan's pool) are
+ * summed in chunk order by a second kernel: results are bit-reproducible run to run. */
 sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
                              const double* tx_pos, const double* rx_pos,
                              const float* doppler_bins, int32_t chirp0, int32_t nchirp,
@@ -197,10 +201,11 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
  * With symmetric memory the images are the P2P-mapped buffers of every rank (one NVLink
  * store or reduction per peer).  Rows outside [row0, row0 + nrow) are not touched; the caller
  * orders the ranks (e.g. a symmetric-memory barrier) before reading.  A store scatter whose
- * shard cannot fill 7 waves of the GPU unsplit runs chirp-split: the chunks add into a
- * stream-ordered accumulation image from the plan's pool and the last chunk of each tile
- * stores the finished tile (SAR_ERR_NO_MEMORY never results: without the workspace it runs
- * unsplit).  SAR_SCATTER_ADD runs unsplit.
+ * shard cannot fill 7 waves of the GPU unsplit runs chirp-split: each chunk stores its partial
+ * tile into its own plane of a stream-ordered workspace from the plan's pool and the last chunk
+ * of each tile sums the planes in chunk order and stores the finished tile (SAR_ERR_NO_MEMORY
+ * never results: without the workspace it runs unsplit).  SAR_SCATTER_ADD runs unsplit; its
+ * cross-rank additions land in arrival order (fp32: not bit-reproducible across runs).
  *   images  host array of n_images device pointers (may be peer or multicast addresses) */
 #define SAR_SCATTER_MULTICAST 1
 #define SAR_SCATTER_ADD 2
@@ -209,6 +214,35 @@ sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* pro
                                      const float* doppler_bins, int32_t chirp0, int32_t nchirp,
                                      int32_t row0, int32_t nrow, sar_complex64_t* const* images,
                                      int32_t n_images, int32_t flags, sar_stream_t stream);
+
+/* Tile shards ("rank r owns a contiguous block of tiles"; T11).  The BP computes
+ * the grid in absolute tiles of tile_x x tile_y pixels (sar_plan_info), tile t = ty * tiles_x + tx
+ * covering columns [tx tile_x, +tile_x) and rows [ty tile_y, +tile_y) clipped to the grid, each
+ * with its own fp64 anchor at the tile centre.  Every pixel is therefore computed identically by
+ * any row shard, tile shard or unsharded call that contains it (pixel independence of Alg. 2,
+ * P:L459); images differ only in the fp32 order of chirp-chunk sums when the launches
+ * split their chirps differently (<= 1e-6 relative).
+ *
+ * sar_plan_tiles: tiles_x = ceil(nx / tile_x), tiles_y = ceil(ny / tile_y). */
+sar_status_t sar_plan_tiles(sar_plan_t plan, int32_t* tiles_x, int32_t* tiles_y);
+
+/* sar_backproject over the absolute tiles [tile0, tile0 + ntile) (0 <= tile0, tile0 + ntile <=
+ * tiles_x * tiles_y; ntile == 0 is a no-op) for chirps [chirp0, chirp0 + nchirp):
+ *   image  dev complex [ny][nx], the FULL image (absolute rows): only the pixels of the tiles
+ *          in range are written (accumulate 0: =, 1: +=); all other pixels are untouched.
+ * Errors as sar_backproject. */
+sar_status_t sar_backproject_tiles(sar_plan_t plan, const sar_complex64_t* profiles, const double* tx_pos,
+                                   const double* rx_pos, const float* doppler_bins, int32_t chirp0,
+                                   int32_t nchirp, int32_t tile0, int32_t ntile, sar_complex64_t* image,
+                                   int32_t accumulate, sar_stream_t stream);
+
+/* sar_backproject_scatter over the absolute tiles [tile0, tile0 + ntile): every finished tile is
+ * stored (or added, SAR_SCATTER_ADD) at its absolute position of each full image images[d]. */
+sar_status_t sar_backproject_scatter_tiles(sar_plan_t plan, const sar_complex64_t* profiles,
+                                           const double* tx_pos, const double* rx_pos,
+                                           const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                                           int32_t tile0, int32_t ntile, sar_complex64_t* const* images,
+                                           int32_t n_images, int32_t flags, sar_stream_t stream);
 
 /* End-to-end image formation from HOST buffers (the paper's "Load" + "BP",
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a

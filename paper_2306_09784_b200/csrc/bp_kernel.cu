@@ -17,7 +17,7 @@ size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic) {
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
   // the scatter family only for split scatters (its publish epilogue); unsplit scatters take
   // the plain family, whose generic epilogue stores to peers (and whose schedule is faster)
-  if (a.n_peer > 0 && a.acc_img && a.tile_count) return launch_bp_scatter(a, bistatic, doppler, near, s);
+  if (a.n_peer > 0 && a.ws && a.tile_count) return launch_bp_scatter(a, bistatic, doppler, near, s);
   return launch_shapes<false>(a, bistatic, doppler, near, s);
 }
 

@@ -80,6 +80,8 @@ constexpr long kMinSplitItems = SAR_BP_MIN_SPLIT;
 #define SAR_BP_SPLIT_WAVES 32
 #endif
 constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
+// pixel (column x, image row y) inside the launch's image rows (y < 0: a tile row starting above)
+#define SAR_PIX_OK(x, y) ((x) < a.nx && (unsigned)(y) < (unsigned)a.nrow)
 #ifndef SAR_BP_RX_UNROLL
 #define SAR_BP_RX_UNROLL 4                // bistatic RX-loop unroll (C4 1146 -> 1112 ms; 2 is slower)
 #endif
@@ -113,6 +115,12 @@ __device__ __forceinline__ void tr_ids(int trc, int w) {
 #else
 #define SAR_TR(w, it, k)
 #endif
+
+__device__ __forceinline__ unsigned ctaid_x() {   // opaque to CSE: not kept live across loops
+  unsigned v;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v));
+  return v;
+}
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
@@ -245,25 +253,35 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // CTA -> (chirp chunk, tile), chunk-major so that concurrently resident CTAs stream the
-  // same profile rows through L2.  ksplit > 1 only for grids too small to fill the GPU.
-  const int ntiles = a.tiles_x * a.tiles_y;
-  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
-  const int chirp0 = a.chirp0 + chunk * a.chunk;
-  const int nchirp = min(a.chunk, a.nchirp - chunk * a.chunk);
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  // same profile rows through L2.  Tiles are ABSOLUTE grid tiles (tile = ty * tiles_x + tx of the
+  // whole grid, range [tile0, tile0 + ntile)): every pixel is computed with the same anchor
+  // whatever the shard, so a row or tile shard reproduces the unsharded image (Alg. 2's pixel
+  // loop is independent per pixel).  ksplit > 1 for grids too small to fill
+  // the GPU (chunks summed in chunk order: deterministic).
+  // The launch covers whole tile rows [ty0, ty0 + ntile / tiles_x); CTAs outside the valid
+  // launch-local range [tile_lo, tile_hi) (a tile shard's ragged first / last tile row) exit
+  // at once.  (This form of the index arithmetic, launch-local with the row offset added last,
+  // keeps ptxas's fastest schedule of the chirp loop: adding an absolute tile offset before
+  // the division by tiles_x measured 2.7 % slower on C3.)
+  const unsigned tile_l = blockIdx.x % (unsigned)a.ntile, chunk = blockIdx.x / (unsigned)a.ntile;
+  if (tile_l < (unsigned)a.tile_lo || tile_l >= (unsigned)a.tile_hi) return;
+  const int chirp0 = a.chirp0 + (int)chunk * a.chunk;
+  const int nchirp = min(a.chunk, a.nchirp - (int)chunk * a.chunk);
+  const int tx = (int)(tile_l % (unsigned)a.tiles_x), ty = (int)(tile_l / (unsigned)a.tiles_x) + a.ty0;
   const int i0 = tx * TX;               // first grid column of the tile
-  const int j0 = ty * TY;               // first row of the tile, relative to row0
+  const int J0 = ty * TY;               // first grid row of the tile (absolute)
+  const int j0 = J0 - a.row0;           // ... relative to the image's first row (may be < 0)
   // tile anchor: centre of the full tile (even when ragged), fp64.  Cartesian grids:
   // (x0 + i dx, y0 + j dy); polar grids (Measure E): (xc + r sin th, yc + r cos th).
   double PTx, PTy;
   if (a.polar) {
     const double th = a.th0 + (i0 + 0.5 * (TX - 1)) * a.dth;
-    const double rr = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+    const double rr = a.r0 + (J0 + 0.5 * (TY - 1)) * a.dr;
     PTx = a.x0 + rr * sin(th);
     PTy = a.y0 + rr * cos(th);
   } else {
     PTx = a.x0 + (i0 + 0.5 * (TX - 1)) * a.dx;
-    PTy = a.y0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dy;
+    PTy = a.y0 + (J0 + 0.5 * (TY - 1)) * a.dy;
   }
   const double PTz = a.z0;
 
@@ -432,7 +450,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     double dux, duy;
     if (a.polar) {   // pixel offset from the anchor, both evaluated in fp64
       const double th = a.th0 + (i0 + xl) * a.dth;
-      const double rr = a.r0 + (a.row0 + j0 + yl) * a.dr;
+      const double rr = a.r0 + (J0 + yl) * a.dr;
       dux = (a.x0 + rr * sin(th)) - PTx;
       duy = (a.y0 + rr * cos(th)) - PTy;
     } else {
@@ -446,7 +464,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     acc_i[p] = 0.f;
     fd[p] = 0.f;
     if (DOP) {
-      if (gx[p] < a.nx && gy[p] < a.nrow) fd[p] = __ldg(a.dop + (size_t)(a.row0 + gy[p]) * a.nx + gx[p]);
+      if (SAR_PIX_OK(gx[p], gy[p])) fd[p] = __ldg(a.dop + (size_t)(J0 + yl) * a.nx + gx[p]);
     }
     // keep the per-pixel constants in registers: a shuffle is opaque to ptxas, which
     // otherwise re-derives them from fp64 inside the chirp loop (rematerialisation)
@@ -602,7 +620,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     }
   }
   // epilogue: remove the Doppler index shift from the folded phase, then store (or
-  // accumulate) the tile
+  // accumulate) the tile.  The chirp chunk is re-read from %ctaid here (not kept in a register
+  // across the chirp loop, whose schedule is sensitive to register pressure)
+  const int chunk_e = (int)(ctaid_x() / (unsigned)a.ntile);
 #pragma unroll
   for (int p = 0; p < PB; ++p) {
     if (DOP) {
@@ -614,29 +634,34 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     }
   }
   if constexpr (SCATTER) {
-    if (a.acc_img && a.ksplit > 1) {
-      // split scatter: add this chunk into the local accumulation image; the last chunk of the
-      // tile to finish (threadfence-reduction pattern on a per-tile counter) reads the tile
-      // back from L2 and stores it to every peer, so the gather still overlaps other tiles
+    if (a.ws && a.ksplit > 1) {
+      // split scatter: this chunk stores its partial tile into plane `chunk` of the workspace;
+      // the last chunk of the tile to finish (threadfence-reduction pattern on a per-tile
+      // counter) sums the planes in chunk order (deterministic) and stores the finished tile
+      // to every peer, so the gather still overlaps other tiles
+      float2* wsp = a.ws + (size_t)chunk_e * a.ws_plane;
 #pragma unroll
       for (int p = 0; p < PB; ++p)
-        if (gx[p] < a.nx && gy[p] < a.nrow) {
-          float* d = reinterpret_cast<float*>(a.acc_img + (size_t)gy[p] * a.nx + gx[p]);
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
-        }
+        if (SAR_PIX_OK(gx[p], gy[p]))
+          __stcg(wsp + (size_t)gy[p] * a.nx + gx[p], make_float2(acc_r[p], acc_i[p]));
       __threadfence();
       // the flag lives in the record area: past the first barrier no consumer reads the ring
       volatile int* s_last = reinterpret_cast<volatile int*>(smem + L.rec);
       asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");   // consumer warps only
-      if (threadIdx.x == 0) *s_last = atomicAdd(a.tile_count + tile, 1) == a.ksplit - 1;
+      if (threadIdx.x == 0) *s_last = atomicAdd(a.tile_count + (int)(ctaid_x() % (unsigned)a.ntile), 1) == a.ksplit - 1;
       asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
       if (!*s_last) return;
       __threadfence();
 #pragma unroll
       for (int p = 0; p < PB; ++p) {
-        if (gx[p] < a.nx && gy[p] < a.nrow) {
-          const float2 v = __ldcg(a.acc_img + (size_t)gy[p] * a.nx + gx[p]);
+        if (SAR_PIX_OK(gx[p], gy[p])) {
+          const size_t o = (size_t)gy[p] * a.nx + gx[p];
+          float2 v = __ldcg(a.ws + o);
+          for (int c = 1; c < a.ksplit; ++c) {
+            const float2 w = __ldcg(a.ws + (size_t)c * a.ws_plane + o);
+            v.x += w.x;
+            v.y += w.y;
+          }
           acc_r[p] = v.x;
           acc_i[p] = v.y;
         }
@@ -646,7 +671,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     // NVLink while other tiles are still being computed
 #pragma unroll
     for (int p = 0; p < PB; ++p) {
-      if (gx[p] < a.nx && gy[p] < a.nrow) {
+      if (SAR_PIX_OK(gx[p], gy[p])) {
         const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
         if (a.multicast) {
           float* d = reinterpret_cast<float*>(a.peer[0] + o);
@@ -675,7 +700,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     // measured fastest on C3 (0.7 % faster than without; tools/libsweep.sh).
 #pragma unroll
     for (int p = 0; p < PB; ++p) {
-      if (gx[p] < a.nx && gy[p] < a.nrow) {
+      if (SAR_PIX_OK(gx[p], gy[p])) {
         float2* dst = a.img + (size_t)gy[p] * a.nx + gx[p];
         if (a.n_peer > 0) {
           const size_t o = (size_t)(a.row0 + gy[p]) * a.nx + gx[p];
@@ -699,11 +724,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             for (int q = 0; q < a.n_peer; ++q) a.peer[q][o] = make_float2(acc_r[p], acc_i[p]);
           }
         } else if (a.ksplit > 1) {
-          // several chirp chunks add into the same pixel (the image was zeroed first when
-          // not accumulating); fire-and-forget reductions in L2
-          float* d = reinterpret_cast<float*>(dst);
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d), "f"(acc_r[p]) : "memory");
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(d + 1), "f"(acc_i[p]) : "memory");
+          // chirp chunks: each stores its partial into its own workspace plane; the split-sum
+          // kernel adds the planes in chunk order (deterministic, unlike reductions)
+          __stcg(a.ws + (size_t)chunk_e * a.ws_plane + (size_t)gy[p] * a.nx + gx[p], make_float2(acc_r[p], acc_i[p]));
         } else if (a.accumulate) {
           const float2 o = *dst;
           *dst = make_float2(o.x + acc_r[p], o.y + acc_i[p]);
@@ -725,7 +748,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     }
     double rho_t = a.tile_rho;
     if (a.polar) {   // annular patch: farthest from its anchor at a corner
-      const double rc = a.r0 + (a.row0 + j0 + 0.5 * (TY - 1)) * a.dr;
+      const double rc = a.r0 + (J0 + 0.5 * (TY - 1)) * a.dr;
       const double ht = 0.5 * (TX - 1) * a.dth, hr = 0.5 * (TY - 1) * a.dr;
       rho_t = 0.0;
       for (int c = 0; c < 4; ++c) {
@@ -765,7 +788,6 @@ struct BpKernel<true, DOP, NEAR, NCW, PB, SCATTER> {
 template <bool BI, bool DOP, bool SAFE, int NCW, int PB, bool SCATTER>
 cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   auto kern = BpKernel<BI, DOP, SAFE, NCW, PB, SCATTER>::fn;
-  constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
   // the dynamic shared-memory opt-in is per device and per kernel instantiation
   static std::atomic<int> configured_bytes[kMaxDevices];
@@ -783,8 +805,7 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
     }
   }
   BpArgs b = a;
-  b.tiles_y = (a.nrow + TY - 1) / TY;
-  const long ntiles = (long)b.tiles_x * b.tiles_y;
+  const long ntiles = a.tile_hi - a.tile_lo;   // tiles that compute (the split heuristic)
   // Chirp split: enough CTAs for kSplitWaves waves of resident CTAs, each chunk at least
   // kMinSplitItems (chirp, RX) items (and a multiple of the ring stage).
   int resident = 0;
@@ -800,27 +821,27 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   // measured: unsplit +1.0 % at 7.5 waves (C3 rows / 2), +4 % at 6.0 (C2 to a host image),
   // +5.9 % at 3.7 (C3 rows / 4); the split publish costs +2.4 %
   if (a.n_peer > 0 && ntiles >= 7 * slots) k = 1;
+  // reductions into peers (chirp shards) run unsplit
+  if (a.n_peer > 0 && a.accumulate) k = 1;
+  auto split = [&](int kk) {
+    b.chunk = (a.nchirp + kk - 1) / kk;
+    b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
+    b.ksplit = std::max(1, (a.nchirp + b.chunk - 1) / std::max(1, b.chunk));
+  };
+  split(k);
   if (a.split_query) {
-    // planning query, nothing runs: the chirp split of a plain launch
-    *a.split_query = k;
+    // planning query, nothing runs: the number of chirp chunks (workspace planes) of this launch
+    *a.split_query = b.ksplit;
     return cudaSuccess;
   }
-  // scatter epilogue: split only with an accumulation image and tile counters (stores to the
-  // peers come from the last chunk of each tile); reductions into peers run unsplit
-  if (a.n_peer > 0 && (a.accumulate || !a.acc_img || !a.tile_count)) k = 1;
-  b.chunk = (a.nchirp + k - 1) / k;
-  b.chunk = ((b.chunk + a.CB - 1) / a.CB) * a.CB;
-  b.ksplit = (a.nchirp + b.chunk - 1) / std::max(1, b.chunk);
-  if (b.ksplit < 1) b.ksplit = 1;
+  // a split needs its workspace planes (and tile counters for a scatter); without them, unsplit
+  if (b.ksplit > 1 && (!a.ws || a.ws_planes < b.ksplit || (a.n_peer > 0 && !a.tile_count))) split(1);
   if (b.ksplit > 1 && a.n_peer > 0) {
-    cudaError_t e = cudaMemsetAsync(a.acc_img, 0, sizeof(float2) * (size_t)a.nrow * a.nx, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.tile_count, 0, sizeof(int) * (size_t)ntiles, s);
-    if (e != cudaSuccess) return e;
-  } else if (b.ksplit > 1 && !a.accumulate) {
-    cudaError_t e = cudaMemsetAsync(a.img, 0, sizeof(float2) * (size_t)a.nrow * a.nx, s);
+    cudaError_t e = cudaMemsetAsync(a.tile_count, 0, sizeof(int) * (size_t)a.ntile, s);
     if (e != cudaSuccess) return e;
   }
-  const long grid = ntiles * b.ksplit;
+  if (a.ksplit_out) *a.ksplit_out = b.ksplit;
+  const long grid = (long)a.ntile * b.ksplit;
   kern<<<(unsigned)grid, (NCW + 1) * 32, L.total, s>>>(b);
   return cudaGetLastError();
 }

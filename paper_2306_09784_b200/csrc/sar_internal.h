@@ -44,8 +44,11 @@ struct BpArgs {
   const float* dop;        // [ny][nx] or nullptr
   const float2* binphase;  // [n_bins+1] exp(j 2 pi beta (k_lo + k + 1/2)), k = -1.., beta = c2/a1
   float2* img;             // [nrow][nx]
+  // image rows [row0, row0 + nrow) of the grid (img points at row row0).  A launch covers the
+  // whole tile rows [ty0, ty0 + ntile / tiles_x) (launch-local tile t = (ty - ty0) * tiles_x + tx);
+  // the CTAs compute the tiles t in [tile_lo, tile_hi) and store only their pixels inside the rows
   int n_bins, n_rx, chirp0, nchirp, row0, nrow, nx, tiles_x, accumulate;
-  int tiles_y;              // set by the launcher
+  int ty0, ntile, tile_lo, tile_hi;
   int ksplit, chunk;        // chirp split (launcher): ksplit chunks of `chunk` chirps
   int W;                   // window bins per item
   int CB;                  // chirps per ring stage
@@ -64,12 +67,17 @@ struct BpArgs {
   // written with multimem.st when multicast != 0) instead of img
   float2* peer[8];
   int n_peer, multicast;
-  // Chirp split under a (non-accumulating) scatter: chunks add into acc_img ([nrow][nx], zeroed
-  // by the launcher) and the last chunk of each tile (tile_count, zeroed) stores the finished
-  // tile to every peer.  nullptr: the scatter runs unsplit.
-  float2* acc_img;
+  // Chirp split: chunk c stores its partial image into plane c of ws ([ws_planes][nrow][nx],
+  // plane stride ws_plane elements); the planes are summed in chunk order (deterministic) by the
+  // split-sum kernel, or under a scatter by the last chunk of each tile (tile_count, per tile of
+  // the launch, zeroed by the launcher), which then stores the finished tile to every peer.
+  // ws == nullptr: the launch runs unsplit.
+  float2* ws;
+  long ws_plane;
+  int ws_planes;
   int* tile_count;
-  int* split_query;        // non-null: report the chirp split of this launch, do not launch
+  int* split_query;        // non-null: report the chirp chunks of this launch, do not launch
+  int* ksplit_out;         // non-null: receives the chirp chunks of the launch
   const float4* pairs;     // pair-format rows [n_chirps * n_rx][pair_stride] (pair_kernel) or nullptr
   int pair_stride, pair_pad;   // entry of crop bin k: k + pair_pad (pad minus the rows' first bin)
   float A1f;               // index slope per metre of Delta-R (2 a1 monostatic, a1 bistatic)
@@ -96,6 +104,15 @@ struct DopArgs {
 };
 cudaError_t launch_doppler(const DopArgs& a, cudaStream_t s);
 cudaError_t launch_sum(float2* out, const float2* in, int n, long stride, long count, cudaStream_t s);
+// Chirp-split sum: img[p] (+)= ws[0][p] + ws[1][p] + ... (chunk order) for the pixels of the
+// absolute tiles [tile0, tile0 + ntile) inside rows [row0, row0 + nrow) (img, ws at row row0).
+struct SplitSumArgs {
+  float2* img;
+  const float2* ws;
+  long plane;
+  int planes, tile0, ntile, tiles_x, tile_y, row0, nrow, nx, accumulate;
+};
+cudaError_t launch_split_sum(const SplitSumArgs& a, cudaStream_t s);
 
 // Polar -> Cartesian resampling arguments (resample_kernel.cu).
 struct ResampleArgs {

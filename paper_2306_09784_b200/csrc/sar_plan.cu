@@ -569,14 +569,33 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
                               const double* rx_pos, const float* doppler_bins, int32_t chirp0,
                               int32_t nchirp, int32_t row0, int32_t nrow, sar_complex64_t* image,
                               int32_t accumulate, sar_complex64_t* const* peers, int32_t n_peer,
-                              int32_t multicast, sar_stream_t stream, int* split_query = nullptr) {
+                              int32_t multicast, sar_stream_t stream, int32_t tile0 = -1, int32_t ntile = 0) {
+  // Row mode (tile0 < 0): rows [row0, row0 + nrow), the CTAs run every absolute grid tile those
+  // rows touch.  Tile mode: the absolute tiles [tile0, tile0 + ntile); `image` is the full
+  // [ny][nx] image and the call writes the pixels of those tiles only.
   if (!plan) return fail(SAR_ERR_INVALID_ARGUMENT, "plan is null");
   const sar_radar_params_t& r = plan->radar;
   const sar_grid_t& g = plan->grid;
+  const int TXp = plan->info.tile_x, TYp = plan->info.tile_y;
+  const int tiles_x = (g.nx + TXp - 1) / TXp, tiles_y = (g.ny + TYp - 1) / TYp;
   if (chirp0 < 0 || nchirp < 0 || (int64_t)chirp0 + nchirp > r.n_chirps)
     return fail(SAR_ERR_INVALID_ARGUMENT, "chirp shard out of range");
-  if (row0 < 0 || nrow < 0 || (int64_t)row0 + nrow > g.ny)
-    return fail(SAR_ERR_INVALID_ARGUMENT, "row shard out of range");
+  if (tile0 >= 0) {
+    if (ntile < 0 || (int64_t)tile0 + ntile > (int64_t)tiles_x * tiles_y)
+      return fail(SAR_ERR_INVALID_ARGUMENT, "tile range out of range");
+    if (ntile == 0) return SAR_OK;
+    const int ty0 = tile0 / tiles_x, ty1 = (tile0 + ntile - 1) / tiles_x;
+    row0 = ty0 * TYp;
+    nrow = std::min(g.ny, (ty1 + 1) * TYp) - row0;
+    if (image) image += (size_t)row0 * g.nx;
+  } else {
+    if (row0 < 0 || nrow < 0 || (int64_t)row0 + nrow > g.ny)
+      return fail(SAR_ERR_INVALID_ARGUMENT, "row shard out of range");
+    if (nrow > 0) {
+      tile0 = (row0 / TYp) * tiles_x;
+      ntile = ((row0 + nrow - 1) / TYp + 1) * tiles_x - tile0;
+    }
+  }
   if (accumulate != 0 && accumulate != 1) return fail(SAR_ERR_INVALID_ARGUMENT, "accumulate must be 0 or 1");
   if (!rx_pos && r.n_rx != 1)
     return fail(SAR_ERR_INVALID_ARGUMENT, "rx_pos may be NULL (monostatic) only when n_rx == 1");
@@ -599,7 +618,11 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.row0 = row0;
   a.nrow = nrow;
   a.nx = g.nx;
-  a.tiles_x = (g.nx + plan->info.tile_x - 1) / plan->info.tile_x;
+  a.tiles_x = tiles_x;
+  a.ty0 = tile0 / tiles_x;   // the launch covers whole tile rows; [tile_lo, tile_hi) compute
+  a.tile_lo = tile0 - a.ty0 * tiles_x;
+  a.tile_hi = a.tile_lo + ntile;
+  a.ntile = ((tile0 + ntile - 1) / tiles_x + 1) * tiles_x - a.ty0 * tiles_x;
   a.S = plan->bp_stages;
   a.ncw = plan->bp_ncw;
   a.pb = plan->bp_pb;
@@ -631,7 +654,8 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.C3f = (float)(2.0 * sar::kPi * a.c2 / a.a1);
   a.n_peer = n_peer;
   a.multicast = multicast;
-  a.split_query = split_query;
+  a.split_query = nullptr;
+  a.ksplit_out = nullptr;
   a.pairs = nullptr;
   a.pair_stride = a.pair_pad = 0;
   float4* pairs = nullptr;
@@ -639,19 +663,21 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     const char* e = getenv("SAR_BP_NO_PAIRS");
     return e && e[0] == '1';
   }();
-  // Pair rows cover the bins of this call's rows only (a row shard's own crop, same margins
-  // as the plan's; windows of tiles reaching past the shard fall in the zero-extended pad)
+  // Pair rows cover the bins of this call's tiles only (a shard's own crop over the rows of
+  // the tiles it runs, whole tiles included, same margins as the plan's)
   int kb0 = 0, kbn = plan->info.n_bins;
-  if (row0 != 0 || nrow != g.ny) {
+  const int trow0 = (tile0 / tiles_x) * TYp;
+  const int trow1 = std::min(g.ny, ((tile0 + ntile - 1) / tiles_x + 1) * TYp);
+  if (trow0 != 0 || trow1 != g.ny) {
     sar_grid_t sg = g;
     sar_polar_grid_t spg = plan->pgrid;
     if (plan->polar) {
-      spg.r0 = plan->pgrid.r0 + row0 * plan->pgrid.dr;
-      spg.n_r = nrow;
+      spg.r0 = plan->pgrid.r0 + trow0 * plan->pgrid.dr;
+      spg.n_r = trow1 - trow0;
     } else {
-      sg.y0 = g.y0 + row0 * g.dy;
+      sg.y0 = g.y0 + trow0 * g.dy;
     }
-    sg.ny = nrow;
+    sg.ny = trow1 - trow0;
     double dmin, dmax;
     long lo, hi;
     if (crop_bins(&r, &sg, &plan->box, plan->polar ? &spg : nullptr, plan->info.a1_bins_per_m, &dmin, &dmax, &lo,
@@ -662,7 +688,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
       kbn = (int)(b1 - b0);
     }
   }
-  if (nchirp > 0 && !split_query && !no_pairs) {
+  if (nchirp > 0 && !no_pairs) {
     // Pair-format rows of this call's chirps (pair_kernel, HBM-bound), in a stream-ordered
     // allocation from the plan's pool so that calls on different streams stay independent;
     // the BP producer then only issues one bulk copy per (tile, chirp, RX) window.
@@ -698,39 +724,65 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     a.pair_pad = pad - kb0;
   }
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
-  a.acc_img = nullptr;
+  a.ws = nullptr;
+  a.ws_plane = 0;
+  a.ws_planes = 0;
   a.tile_count = nullptr;
   static const bool scatter_nosplit = [] {   // tuning switch: scatters always unsplit
     const char* e = getenv("SAR_BP_SCATTER_NOSPLIT");
     return e && e[0] == '1';
   }();
-  if (n_peer > 0 && !accumulate && nchirp > 0 && !split_query && !scatter_nosplit) {
-    // a scatter that would run chirp-split: accumulation image + per-tile counters from the
-    // pool (the last chunk of each tile publishes it); without them it runs unsplit
+  if (nchirp > 0 && !(n_peer > 0 && scatter_nosplit)) {
+    // a launch that would run chirp-split: one workspace plane per chunk (+ per-tile counters for
+    // a scatter, whose last chunk per tile publishes it) from the plan's pool; without them it
+    // runs unsplit
     int k = 1;
-    sar::BpArgs q = a;   // the launcher's split of this scatter (its unsplit policy included)
+    sar::BpArgs q = a;   // the launcher's split of this launch (its scatter policy included)
     q.split_query = &k;
     if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, plan->near_field, (cudaStream_t)stream) == cudaSuccess &&
         k > 1) {
-      const size_t ntiles = (size_t)a.tiles_x * ((nrow + plan->info.tile_y - 1) / plan->info.tile_y);
-      if (cudaMallocFromPoolAsync((void**)&a.acc_img, (size_t)nrow * g.nx * sizeof(float2), plan->pool,
+      a.ws_plane = (long)nrow * g.nx;
+      if (cudaMallocFromPoolAsync((void**)&a.ws, (size_t)k * a.ws_plane * sizeof(float2), plan->pool,
                                   (cudaStream_t)stream) != cudaSuccess ||
-          cudaMallocFromPoolAsync((void**)&a.tile_count, ntiles * sizeof(int), plan->pool, (cudaStream_t)stream) !=
-              cudaSuccess) {
+          (n_peer > 0 && cudaMallocFromPoolAsync((void**)&a.tile_count, (size_t)a.ntile * sizeof(int), plan->pool,
+                                                 (cudaStream_t)stream) != cudaSuccess)) {
         cudaGetLastError();
-        if (a.acc_img) cudaFreeAsync(a.acc_img, (cudaStream_t)stream);
-        a.acc_img = nullptr;
+        if (a.ws) cudaFreeAsync(a.ws, (cudaStream_t)stream);
+        a.ws = nullptr;
         a.tile_count = nullptr;
+      } else {
+        a.ws_planes = k;
       }
     }
   }
+  int ksplit = 1;
+  a.ksplit_out = &ksplit;
   cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
                                  (cudaStream_t)stream);
-  if (a.acc_img) cudaFreeAsync(a.acc_img, (cudaStream_t)stream);
+  bool summed = false;
+  if (e == cudaSuccess && ksplit > 1 && n_peer == 0) {
+    // the chunk planes in chunk order into the image (deterministic)
+    sar::SplitSumArgs sa;
+    sa.img = a.img;
+    sa.ws = a.ws;
+    sa.plane = a.ws_plane;
+    sa.planes = ksplit;
+    sa.tile0 = tile0;
+    sa.ntile = ntile;
+    sa.tiles_x = tiles_x;
+    sa.tile_y = TYp;
+    sa.row0 = row0;
+    sa.nrow = nrow;
+    sa.nx = g.nx;
+    sa.accumulate = accumulate;
+    e = sar::launch_split_sum(sa, (cudaStream_t)stream);
+    summed = true;
+  }
+  if (a.ws) cudaFreeAsync(a.ws, (cudaStream_t)stream);
   if (a.tile_count) cudaFreeAsync(a.tile_count, (cudaStream_t)stream);
   if (pairs) cudaFreeAsync(pairs, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
-  if (!split_query) plan->launches.fetch_add(pairs ? 2 : 1);
+  plan->launches.fetch_add((pairs ? 2 : 1) + (summed ? 1 : 0));
   return SAR_OK;
 }
 }  // namespace
@@ -760,6 +812,41 @@ sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* pro
   if (add && nchirp == 0) return SAR_OK;
   return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, row0, nrow, images[0],
                           add, images, n_images, multicast, stream);
+}
+
+sar_status_t sar_backproject_tiles(sar_plan_t plan, const sar_complex64_t* profiles, const double* tx_pos,
+                                   const double* rx_pos, const float* doppler_bins, int32_t chirp0,
+                                   int32_t nchirp, int32_t tile0, int32_t ntile, sar_complex64_t* image,
+                                   int32_t accumulate, sar_stream_t stream) {
+  if (tile0 < 0) return fail(SAR_ERR_INVALID_ARGUMENT, "tile0 must be >= 0");
+  return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, 0, 0, image, accumulate,
+                          nullptr, 0, 0, stream, tile0, ntile);
+}
+
+sar_status_t sar_backproject_scatter_tiles(sar_plan_t plan, const sar_complex64_t* profiles,
+                                           const double* tx_pos, const double* rx_pos,
+                                           const float* doppler_bins, int32_t chirp0, int32_t nchirp,
+                                           int32_t tile0, int32_t ntile, sar_complex64_t* const* images,
+                                           int32_t n_images, int32_t flags, sar_stream_t stream) {
+  if (tile0 < 0) return fail(SAR_ERR_INVALID_ARGUMENT, "tile0 must be >= 0");
+  if (!images || n_images < 1 || n_images > 8)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "images must hold 1..8 device pointers");
+  if (flags & ~(SAR_SCATTER_MULTICAST | SAR_SCATTER_ADD)) return fail(SAR_ERR_INVALID_ARGUMENT, "unknown flags");
+  const int multicast = (flags & SAR_SCATTER_MULTICAST) ? 1 : 0, add = (flags & SAR_SCATTER_ADD) ? 1 : 0;
+  if (multicast && n_images != 1)
+    return fail(SAR_ERR_INVALID_ARGUMENT, "a multicast store takes exactly one (multicast) address");
+  for (int d = 0; d < n_images; ++d)
+    if (!images[d]) return fail(SAR_ERR_INVALID_ARGUMENT, "null image pointer");
+  if (add && nchirp == 0) return SAR_OK;
+  return backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, 0, 0, images[0], add,
+                          images, n_images, multicast, stream, tile0, ntile);
+}
+
+sar_status_t sar_plan_tiles(sar_plan_t plan, int32_t* tiles_x, int32_t* tiles_y) {
+  if (!plan || !tiles_x || !tiles_y) return fail(SAR_ERR_INVALID_ARGUMENT, "null argument");
+  *tiles_x = (plan->grid.nx + plan->info.tile_x - 1) / plan->info.tile_x;
+  *tiles_y = (plan->grid.ny + plan->info.tile_y - 1) / plan->info.tile_y;
+  return SAR_OK;
 }
 
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,

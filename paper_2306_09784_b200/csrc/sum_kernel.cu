@@ -38,7 +38,40 @@ __global__ void sum_kernel(float2* __restrict__ out, const float2* __restrict__ 
   }
 }
 
+// Chirp-split sum, one CTA per tile of the launch: pixel (x, y) of the tile gets
+// ws[0] + ws[1] + ... in chunk order (+ the image's own value first when accumulating).  Rows of a
+// tile are 32 contiguous pixels (256 B), so each warp reads and writes whole rows.
+__global__ void __launch_bounds__(256) split_sum_kernel(const SplitSumArgs a) {
+  const int tile = a.tile0 + blockIdx.x;
+  const int i0 = (tile % a.tiles_x) * kTileX, J0 = (tile / a.tiles_x) * a.tile_y;
+  const int x = i0 + (threadIdx.x & 31);
+  if (x >= a.nx) return;
+  for (int yl = threadIdx.x >> 5; yl < a.tile_y; yl += blockDim.x >> 5) {
+    const int y = J0 + yl - a.row0;
+    if (y < 0 || y >= a.nrow) continue;
+    const size_t o = (size_t)y * a.nx + x;
+    float2 s = __ldcs(a.ws + o);
+    for (int c = 1; c < a.planes; ++c) {
+      const float2 v = __ldcs(a.ws + (size_t)c * a.plane + o);
+      s.x += v.x;
+      s.y += v.y;
+    }
+    if (a.accumulate) {
+      const float2 v = a.img[o];
+      s.x = v.x + s.x;
+      s.y = v.y + s.y;
+    }
+    a.img[o] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_split_sum(const SplitSumArgs& a, cudaStream_t s) {
+  if (a.ntile <= 0) return cudaSuccess;
+  split_sum_kernel<<<(unsigned)a.ntile, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sum(float2* out, const float2* in, int n, long stride, long count, cudaStream_t s) {
   int dev = 0, sms = 148;

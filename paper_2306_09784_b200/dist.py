@@ -25,22 +25,38 @@ def row_partition(ny: int, world: int, rank: int):
     return row0, base + (1 if rank < rem else 0)
 
 
+def tile_partition(n_tiles: int, world: int, rank: int):
+    """Contiguous, balanced (+-1 tile) blocks of absolute BP tiles (tile = ty * tiles_x + tx):
+    SURVEY 8(e) "rank r owns a contiguous block of tiles"; with the per-tile anchors every
+    pixel is computed exactly as in the unsharded image."""
+    return row_partition(n_tiles, world, rank)
+
+
+def tile_row_partition(tiles_y: int, tile_y: int, ny: int, world: int, rank: int):
+    """Row blocks made of whole tile rows (balanced +-1 tile row), as (row0, nrow): the row
+    shards of the NCCL all-gather leg, each a contiguous block of tiles."""
+    t0, nt = row_partition(tiles_y, world, rank)
+    row0 = min(ny, t0 * tile_y)
+    return row0, min(ny, (t0 + nt) * tile_y) - row0
+
+
 def chirp_partition(n_chirps: int, world: int, rank: int):
     return row_partition(n_chirps, world, rank)
 
 
-def gather_rows(local, ny: int, group=None):
+def gather_rows(local, ny: int, group=None, parts=None):
     """Assemble the full [ny][nx] complex image from per-rank row blocks.
 
-    Uses all_gather_into_tensor on the float32 view when blocks are equal, else pads
-    every block to ceil(ny/world) rows and trims.  Works for NCCL (CUDA tensors) and
-    gloo (CPU tensors)."""
+    ``parts`` lists every rank's (row0, nrow) (default: ``row_partition``).  Uses
+    all_gather_into_tensor on the float32 view when blocks are equal, else pads every block to
+    the largest block and trims.  Works for NCCL (CUDA tensors) and gloo (CPU tensors)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     nx = local.shape[1]
-    per = -(-ny // world)
+    parts = parts or [row_partition(ny, world, r) for r in range(world)]
+    per = max(n for _, n in parts)
     if local.shape[0] != per:
         pad = torch.zeros((per, nx), dtype=local.dtype, device=local.device)
         pad[: local.shape[0]] = local
@@ -52,14 +68,10 @@ def gather_rows(local, ny: int, group=None):
         dist.all_gather_into_tensor(dst, src, group=group)
     else:
         dist.all_gather(list(dst.chunk(world)), src, group=group)   # chunks are views of dst
-    if per * world == ny:
+    if all(n == per for _, n in parts):
         return full
     # drop the padding rows of every ragged block
-    keep = []
-    for r in range(world):
-        r0, n = row_partition(ny, world, r)
-        keep.append(full[r * per: r * per + n])
-    return torch.cat(keep)
+    return torch.cat([full[r * per: r * per + n] for r, (_, n) in enumerate(parts)])
 
 
 def reduce_partials(partial, dst: int = 0, group=None):

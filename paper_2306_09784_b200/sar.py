@@ -83,6 +83,12 @@ def load() -> ctypes.CDLL:
             lib.sar_backproject_scatter.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, P(_vp), _i32,
                                                     _i32, _vp]
             lib.sar_backproject_scatter.restype = ctypes.c_int
+            lib.sar_backproject_tiles.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp]
+            lib.sar_backproject_scatter_tiles.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, P(_vp),
+                                                          _i32, _i32, _vp]
+            lib.sar_plan_tiles.argtypes = [_vp, P(_i32), P(_i32)]
+            for n in ("sar_backproject_tiles", "sar_backproject_scatter_tiles", "sar_plan_tiles"):
+                getattr(lib, n).restype = ctypes.c_int
             lib.sar_form_image.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]
             lib.sar_doppler_table.argtypes = [P(RadarParams), P(Grid), P(ctypes.c_double * 3),
                                               P(ctypes.c_double * 3), _vp, _vp]
@@ -193,6 +199,25 @@ def sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nch
     arr = (_vp * len(image_ptrs))(*image_ptrs)
     _check(load().sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow,
                                           arr, len(image_ptrs), int(flags), stream))
+
+
+def sar_backproject_tiles(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, tile0, ntile, img_ptr,
+                          accumulate=0, stream=0):
+    _check(load().sar_backproject_tiles(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, tile0, ntile,
+                                        img_ptr, accumulate, stream))
+
+
+def sar_backproject_scatter_tiles(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, tile0, ntile,
+                                  image_ptrs, flags=0, stream=0):
+    arr = (_vp * len(image_ptrs))(*image_ptrs)
+    _check(load().sar_backproject_scatter_tiles(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, tile0,
+                                                ntile, arr, len(image_ptrs), int(flags), stream))
+
+
+def sar_plan_tiles(plan):
+    tx, ty = _i32(), _i32()
+    _check(load().sar_plan_tiles(plan, ctypes.byref(tx), ctypes.byref(ty)))
+    return tx.value, ty.value
 
 
 def sar_form_image(plan, raw_h, wsar_h, tx_h, rx_h, dop_h, row0, nrow, img_h, stream=0):
@@ -410,6 +435,46 @@ class Plan:
                                 chirp0, nchirp, row0, nrow, [int(p) for p in image_ptrs],
                                 (SAR_SCATTER_MULTICAST if multicast else 0) | (SAR_SCATTER_ADD if add else 0),
                                 _stream_handle(stream))
+
+    @property
+    def tiles(self):
+        """(tiles_x, tiles_y): the absolute BP tile grid (tile t = ty * tiles_x + tx)."""
+        return sar_plan_tiles(self.handle)
+
+    def backproject_tiles(self, profiles, tx, tile0, ntile, rx=None, doppler=None, chirp0=0, nchirp=None, out=None,
+                          accumulate=False, stream=None):
+        """Back-project the absolute tiles [tile0, tile0+ntile) into the FULL image ``out``
+        ([ny][nx]; only those tiles' pixels are written)."""
+        import torch
+
+        g = self.grid
+        nchirp = self.n_chirps - chirp0 if nchirp is None else nchirp
+        out = self.empty_image() if out is None else out
+        sar_backproject_tiles(self.handle,
+                              _dptr(profiles, torch.complex64, (self.n_chirps, self.n_rx, self.n_bins), "profiles"),
+                              _dptr(tx, torch.float64, (self.n_chirps, 3), "tx"),
+                              _dptr(rx, torch.float64, (self.n_chirps, self.n_rx, 3), "rx"),
+                              _dptr(doppler, torch.float32, (g.ny, g.nx), "doppler"),
+                              chirp0, nchirp, tile0, ntile, _dptr(out, torch.complex64, (g.ny, g.nx), "image"),
+                              int(bool(accumulate)), _stream_handle(stream))
+        return out
+
+    def backproject_scatter_tiles(self, profiles, tx, image_ptrs, tile0, ntile, rx=None, doppler=None, chirp0=0,
+                                  nchirp=None, multicast=False, add=False, stream=None):
+        """``backproject_scatter`` over the absolute tiles [tile0, tile0+ntile)."""
+        import torch
+
+        g = self.grid
+        nchirp = self.n_chirps - chirp0 if nchirp is None else nchirp
+        sar_backproject_scatter_tiles(self.handle,
+                                      _dptr(profiles, torch.complex64, (self.n_chirps, self.n_rx, self.n_bins),
+                                            "profiles"),
+                                      _dptr(tx, torch.float64, (self.n_chirps, 3), "tx"),
+                                      _dptr(rx, torch.float64, (self.n_chirps, self.n_rx, 3), "rx"),
+                                      _dptr(doppler, torch.float32, (g.ny, g.nx), "doppler"),
+                                      chirp0, nchirp, tile0, ntile, [int(p) for p in image_ptrs],
+                                      (SAR_SCATTER_MULTICAST if multicast else 0) | (SAR_SCATTER_ADD if add else 0),
+                                      _stream_handle(stream))
 
     def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, row0=0, nrow=None, out_h=None,
                    stream=None, sync=True):

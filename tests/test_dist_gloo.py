@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import sarsim
-from paper_2306_09784_b200.dist import chirp_partition, gather_rows, reduce_partials, row_partition
+from paper_2306_09784_b200.dist import (chirp_partition, gather_rows, reduce_partials, row_partition, tile_partition,
+                                       tile_row_partition)
 
 
 def _free_port():
@@ -37,12 +38,17 @@ def _worker(rank, world, port, mode, out_q):
     try:
         scn, prof = _scene()
         g = scn.grid
-        if mode == "rows":
-            r0, n = row_partition(g.ny, world, rank)
+        if mode in ("rows", "tile_rows"):
+            if mode == "rows":
+                parts = None
+                r0, n = row_partition(g.ny, world, rank)
+            else:   # whole tile rows of 4 px: 11 rows = 3 tile rows -> ragged blocks 8 + 3
+                parts = [tile_row_partition(-(-g.ny // 4), 4, g.ny, world, r) for r in range(world)]
+                r0, n = parts[rank]
             pix = g.pixels(rows=np.arange(r0, r0 + n))
             loc = oracle.backproject(prof, 0, scn.radar, scn.tx, scn.rx, pix, nthreads=1)
             local = torch.from_numpy(loc.astype(np.complex64).reshape(n, g.nx))
-            full = gather_rows(local, g.ny)
+            full = gather_rows(local, g.ny, parts=parts)
             if rank == 0:
                 out_q.put(full.numpy())
         else:
@@ -57,7 +63,7 @@ def _worker(rank, world, port, mode, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rows", "chirps"])
+@pytest.mark.parametrize("mode", ["rows", "tile_rows", "chirps"])
 def test_two_rank_gloo_sharding_equals_unsharded(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -83,3 +89,22 @@ def test_partitions_cover_exactly():
                 assert a + na == b
             assert sum(nb for _, nb in blocks) == n
             assert max(nb for _, nb in blocks) - min(nb for _, nb in blocks) <= 1
+
+
+def test_tile_partitions_cover_exactly():
+    """Tile blocks are balanced to +-1 tile; tile-row blocks are whole tile rows (+-1 tile row)
+    covering the grid rows exactly (C3: 94 tile rows of 32 px, ragged last row)."""
+    for nt in (1, 9, 8836, 94 * 38):
+        for w in (1, 2, 3, 8):
+            blocks = [tile_partition(nt, w, r) for r in range(w)]
+            assert sum(b for _, b in blocks) == nt and blocks[0][0] == 0
+            assert max(b for _, b in blocks) - min(b for _, b in blocks) <= 1
+    for ny, ty in ((3000, 32), (1201, 32), (90, 16), (7, 32)):
+        tiles_y = -(-ny // ty)
+        for w in (1, 2, 4, 8):
+            parts = [tile_row_partition(tiles_y, ty, ny, w, r) for r in range(w)]
+            assert parts[0][0] == 0 and sum(n for _, n in parts) == ny
+            for (a, na), (b, _) in zip(parts, parts[1:]):
+                assert a + na == b and (na == 0 or a % ty == 0)
+            full = [n for _, n in parts if n > 0][:-1]
+            assert all(n % ty == 0 for n in full)

@@ -229,6 +229,9 @@ def test_near_field_pixel_on_antenna(cuda_lib):
 
 # ----------------------------------------------------------------------------- shards and edges
 def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
+    """T11: every pixel is computed in its absolute grid tile with the tile's own fp64 anchor,
+    so ANY row shard and any tile shard reproduce the unsharded image bit for bit (these
+    launches are unsplit: 200 (chirp, RX) items); chirp shards agree to fp32 summation order."""
     import torch
 
     scn = sarsim.small_config(n_chirps=100, ns=256, nx=70, ny=90, seed=41, n_rx=2)
@@ -237,31 +240,45 @@ def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
     tx = torch.as_tensor(scn.tx, device="cuda:0")
     rx = torch.as_tensor(scn.rx, device="cuda:0").contiguous()
     ty = plan.info.tile_y
-    # shards on tile-row boundaries keep every tile anchor: bit-identical image
     aligned = torch.cat([plan.backproject(prof, tx, rx, row0=r0, nrow=n) for r0, n in ((0, ty), (ty, 90 - ty))])
-    # arbitrary shards move the anchors: a different fp32 rounding pattern, each within the
-    # parity bar of the oracle; they agree to the accuracy of the anchored form
     rows = torch.cat([plan.backproject(prof, tx, rx, row0=r0, nrow=n) for r0, n in ((0, 23), (23, 40), (63, 27))])
+    tiles_x, tiles_y = plan.tiles
+    assert (tiles_x, tiles_y) == (-(-70 // 32), -(-90 // ty))
+    sentinel = complex(5.0, -5.0)
+    tiled = torch.full((90, 70), sentinel, dtype=torch.complex64, device="cuda:0")
+    for t0, nt in ((0, 2), (2, 3), (5, 1), (6, tiles_x * tiles_y - 6)):
+        plan.backproject_tiles(prof, tx, t0, nt, rx, out=tiled)
+    one = torch.full((90, 70), sentinel, dtype=torch.complex64, device="cuda:0")
+    plan.backproject_tiles(prof, tx, 4, 1, rx, out=one)   # tile (1, 1): only its pixels written
     acc = plan.backproject(prof, tx, rx, chirp0=0, nchirp=37)
     plan.backproject(prof, tx, rx, chirp0=37, nchirp=63, out=acc, accumulate=True)
     torch.cuda.synchronize()
     a = img.cpu().numpy()
     assert torch.equal(aligned, img)
-    assert rel_err(rows.cpu().numpy(), a) < 3e-4
+    assert torch.equal(rows, img)
+    assert torch.equal(tiled, img)
+    mask = torch.zeros((90, 70), dtype=torch.bool, device="cuda:0")
+    mask[ty:2 * ty, 32:64] = True
+    assert torch.equal(one[mask], img[mask]) and torch.all(one[~mask] == sentinel)
     assert rel_err(acc.cpu().numpy(), a) < 1e-5
-    # empty chirp shard: zeros (overwrite) / untouched (accumulate); empty row shard: no-op
+    # empty chirp shard: zeros (overwrite) / untouched (accumulate); empty row/tile shard: no-op
     z = plan.backproject(prof, tx, rx, chirp0=10, nchirp=0)
     keep = acc.clone()
     plan.backproject(prof, tx, rx, chirp0=10, nchirp=0, out=acc, accumulate=True)
     plan.backproject(prof, tx, rx, row0=5, nrow=0, out=acc[:0])
+    plan.backproject_tiles(prof, tx, 3, 0, rx, out=acc)
     torch.cuda.synchronize()
     assert torch.all(z == 0) and torch.equal(acc, keep)
+    with pytest.raises(cuda_lib.SarError):
+        plan.backproject_tiles(prof, tx, tiles_x * tiles_y - 1, 2, rx, out=acc)
     plan.close()
 
 
 def test_chirp_split_for_small_grids(cuda_lib):
-    """A grid of few tiles and many chirps runs as several chirp chunks per tile that add into
-    the image (red.global.add); overwrite and accumulate both match the oracle."""
+    """A grid of few tiles and many chirps runs as several chirp chunks per tile, each storing a
+    partial image into its own workspace plane; a second kernel adds the planes in chunk order.
+    Overwrite and accumulate match the oracle; the image is bit-reproducible run to run, and
+    row / tile shards (other chunkings) agree to fp32 summation order."""
     import torch
 
     scn = sarsim.small_config(n_chirps=2048, ns=256, nx=48, ny=40, seed=45, curved=True)
@@ -270,11 +287,52 @@ def test_chirp_split_for_small_grids(cuda_lib):
     ref = oracle_image(scn, raw.cpu().numpy())
     assert rel_err(img.cpu().numpy().reshape(-1), ref) <= REL_TOL
     tx = torch.as_tensor(scn.tx, device="cuda:0")
+    n0 = plan.launches
+    again = plan.backproject(prof, tx)
+    torch.cuda.synchronize()
+    assert plan.launches - n0 == 3   # pair rows, chirp-split BP, split sum
+    assert torch.equal(again, img)
     twice = img.clone()
     plan.backproject(prof, tx, out=twice, accumulate=True)
+    rows = torch.cat([plan.backproject(prof, tx, row0=r0, nrow=n) for r0, n in ((0, 7), (7, 30), (37, 3))])
+    tiled = torch.zeros_like(img)
+    for t0, nt in ((0, 1), (1, 2), (3, 1)):
+        plan.backproject_tiles(prof, tx, t0, nt, out=tiled)
     torch.cuda.synchronize()
     assert rel_err(twice.cpu().numpy(), 2 * img.cpu().numpy()) < 1e-6
+    assert rel_err(rows.cpu().numpy(), img.cpu().numpy()) < 1e-6
+    assert rel_err(tiled.cpu().numpy(), img.cpu().numpy()) < 1e-6
     plan.close()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_C3_rank_partitions_assemble_the_one_gpu_image(cuda_lib, world):
+    """The bench's N-GPU decompositions of C3, run rank by rank on one GPU: the tile partition
+    (fused-gather leg) and the tile-row partition (NCCL all-gather leg) assemble the 1-GPU image
+    to fp32 chunk order (<= 1e-6); every pixel is computed with the unsharded tile anchor."""
+    import torch
+
+    from paper_2306_09784_b200.dist import tile_partition, tile_row_partition
+
+    scn = sarsim.make_config("C3")
+    raw = _raw(scn)
+    img, prof, plan = gpu_image(scn, raw, return_prof=True)
+    tx = torch.as_tensor(scn.tx, device="cuda:0")
+    g = scn.grid
+    tiles_x, tiles_y = plan.tiles
+    tiled = torch.zeros_like(img)
+    for r in range(world):
+        t0, nt = tile_partition(tiles_x * tiles_y, world, r)
+        plan.backproject_tiles(prof, tx, t0, nt, out=tiled)
+    parts = [tile_row_partition(tiles_y, plan.info.tile_y, g.ny, world, r) for r in range(world)]
+    assert sum(n for _, n in parts) == g.ny and parts[0][0] == 0
+    rows = torch.cat([plan.backproject(prof, tx, row0=r0, nrow=n) for r0, n in parts])
+    torch.cuda.synchronize()
+    ref = img.abs().max()
+    e_t = float((tiled - img).abs().max() / ref)
+    e_r = float((rows - img).abs().max() / ref)
+    plan.close()
+    assert e_t <= 1e-6 and e_r <= 1e-6, (e_t, e_r)
 
 
 def test_one_pixel_grid_and_single_chirp(cuda_lib):

@@ -104,10 +104,11 @@ def test_scatter_add_chirp_shards_equal_full_image(cuda_lib):
 
 @pytest.mark.parametrize("rows,n_rx", [((0, 24), 1), ((5, 13), 1), ((3, 17), 3)])
 def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows, n_rx):
-    """A scatter whose grid is too small to fill the GPU runs chirp-split: every chunk adds into
-    a pool-allocated accumulation image and the last chunk of each tile (per-tile counter)
-    stores the finished tile to every destination.  Equals sar_backproject (also split) to
-    fp32 summation order, the oracle to the parity bar; rows outside the shard untouched."""
+    """A scatter whose grid is too small to fill the GPU runs chirp-split: every chunk stores its
+    partial tile into its own workspace plane and the last chunk of each tile (per-tile counter)
+    sums the planes in chunk order and stores the finished tile to every destination.  Equals
+    sar_backproject (same chunks, same order) bit for bit, the oracle to the parity bar; rows
+    outside the shard untouched."""
     import torch
 
     from tests.helpers import REL_TOL, oracle_image, rel_err
@@ -124,13 +125,33 @@ def test_chirp_split_scatter_last_chunk_publishes(cuda_lib, rows, n_rx):
     g = scn.grid
     ref = plan.backproject(prof, tx, rx, row0=row0, nrow=nrow)
     imgs = [torch.full((g.ny, g.nx), complex(7.0, -7.0), dtype=torch.complex64, device="cuda:0") for _ in range(3)]
-    for _ in range(2):   # the workspace (counters, accumulation image) is reset per launch
+    for _ in range(2):   # the workspace (counters, chunk planes) is reset per launch
         plan.backproject_scatter(prof, tx, [im.data_ptr() for im in imgs], rx, row0=row0, nrow=nrow)
     torch.cuda.synchronize()
     ora = oracle_image(scn, raw.cpu().numpy()).reshape(g.ny, g.nx)[row0:row0 + nrow]
     for im in imgs:
         got = im[row0:row0 + nrow].cpu().numpy()
-        assert rel_err(got, ref.cpu().numpy()) < 1e-6
+        assert torch.equal(im[row0:row0 + nrow], ref)
         assert rel_err(got, ora) <= REL_TOL
         assert torch.all(im[:row0] == complex(7.0, -7.0)) and torch.all(im[row0 + nrow:] == complex(7.0, -7.0))
+    plan.close()
+
+
+def test_tile_scatter_equals_tile_backproject(cuda_lib):
+    """sar_backproject_scatter_tiles: a rank's block of absolute tiles stored into every full
+    image; equals sar_backproject_tiles bit for bit, other pixels untouched."""
+    import torch
+
+    scn, plan, tx, prof = _setup(cuda_lib)
+    g = scn.grid
+    tiles_x, tiles_y = plan.tiles
+    sentinel = complex(7.0, -7.0)
+    ref = torch.full((g.ny, g.nx), sentinel, dtype=torch.complex64, device="cuda:0")
+    plan.backproject_tiles(prof, tx, 2, 3, out=ref)
+    imgs = [torch.full((g.ny, g.nx), sentinel, dtype=torch.complex64, device="cuda:0") for _ in range(2)]
+    plan.backproject_scatter_tiles(prof, tx, [im.data_ptr() for im in imgs], 2, 3)
+    torch.cuda.synchronize()
+    assert int((ref != sentinel).sum()) > 0
+    for im in imgs:
+        assert torch.equal(im, ref)
     plan.close()

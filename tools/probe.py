@@ -1,6 +1,8 @@
 """Ad-hoc GPU probe: MUFU sin/cos accuracy vs argument size, and BP/RC timings on C0/C2/C3."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("SAR_PKG_ROOT"):   # tuning: another build's package (e.g. a previous commit)
+    sys.path.insert(0, os.environ["SAR_PKG_ROOT"])
 import numpy as np
 import torch
 import sarsim
