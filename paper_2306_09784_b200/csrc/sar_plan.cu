@@ -312,6 +312,7 @@ void free_plan(sar_plan_s* p) {
   cudaFree(p->w_dop);
   cudaFree(p->w_prof);
   cudaFree(p->w_img);
+  if (p->side) cudaStreamDestroy(p->side);
   delete p;
 }
 
@@ -565,6 +566,65 @@ sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* 
 }
 
 namespace {
+// A contiguous run of absolute tiles launched on one kernel family (near: the kernel with the
+// per-tile near-field branch).
+struct TileRun {
+  int tile0, ntile;
+  bool near;
+};
+
+// Would the BP kernel's per-tile near-field test (bp_kernel.cuh: anchor within 3 rho_T of the
+// antenna box) take the SAFE form for tile (tx, ty)?  Same fp64 formulas, with a 0.1 % margin so
+// that a tile the kernel would call near is never sent to the fast kernel.
+bool tile_is_near(const sar_plan_t plan, int tx, int ty) {
+  const int TX = plan->info.tile_x, TY = plan->info.tile_y;
+  double pt[3], rho_t = plan->tile_rho;
+  if (plan->polar) {
+    const sar_polar_grid_t& pg = plan->pgrid;
+    const double th = pg.th0 + (tx * TX + 0.5 * (TX - 1)) * pg.dth;
+    const double rc = pg.r0 + (ty * TY + 0.5 * (TY - 1)) * pg.dr;
+    pt[0] = pg.xc + rc * sin(th);
+    pt[1] = pg.yc + rc * cos(th);
+    pt[2] = pg.zc;
+    const double ht = 0.5 * (TX - 1) * pg.dth, hr = 0.5 * (TY - 1) * pg.dr;
+    rho_t = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      const double rr = rc + ((c & 1) ? hr : -hr), dt = (c & 2) ? ht : -ht;
+      rho_t = std::max(rho_t, sqrt(rr * rr + rc * rc - 2.0 * rr * rc * cos(dt)));
+    }
+  } else {
+    const sar_grid_t& g = plan->grid;
+    pt[0] = g.x0 + (tx * TX + 0.5 * (TX - 1)) * g.dx;
+    pt[1] = g.y0 + (ty * TY + 0.5 * (TY - 1)) * g.dy;
+    pt[2] = g.z0;
+  }
+  double d2 = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const double gap = std::max(0.0, std::max(plan->box.lo[k] - pt[k], pt[k] - plan->box.hi[k]));
+    d2 += gap * gap;
+  }
+  const double near_r = (3.0 * rho_t * (1.0 + 1e-6) + 1e-3) * 1.001 + 1e-6;
+  return d2 < near_r * near_r;
+}
+
+// Split [tile0, tile0 + ntile) into runs of near-field / far-field tiles (plans without
+// near-field tiles: one far run).  Many short runs (an antenna box inside the grid) fall back
+// to one run on the near-field kernel, which tests every tile itself.
+std::vector<TileRun> tile_runs(const sar_plan_t plan, int tile0, int ntile, int tiles_x) {
+  std::vector<TileRun> runs;
+  if (!plan->near_field) {
+    runs.push_back({tile0, ntile, false});
+    return runs;
+  }
+  for (int t = tile0; t < tile0 + ntile; ++t) {
+    const bool nr = tile_is_near(plan, t % tiles_x, t / tiles_x);
+    if (!runs.empty() && runs.back().near == nr) ++runs.back().ntile;
+    else runs.push_back({t, 1, nr});
+  }
+  if (runs.size() > 8) runs.assign(1, TileRun{tile0, ntile, true});
+  return runs;
+}
+
 sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, const double* tx_pos,
                               const double* rx_pos, const float* doppler_bins, int32_t chirp0,
                               int32_t nchirp, int32_t row0, int32_t nrow, sar_complex64_t* image,
@@ -618,11 +678,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.row0 = row0;
   a.nrow = nrow;
   a.nx = g.nx;
-  a.tiles_x = tiles_x;
-  a.ty0 = tile0 / tiles_x;   // the launch covers whole tile rows; [tile_lo, tile_hi) compute
-  a.tile_lo = tile0 - a.ty0 * tiles_x;
-  a.tile_hi = a.tile_lo + ntile;
-  a.ntile = ((tile0 + ntile - 1) / tiles_x + 1) * tiles_x - a.ty0 * tiles_x;
+  a.tiles_x = tiles_x;   // (tile ranges per launch below)
   a.S = plan->bp_stages;
   a.ncw = plan->bp_ncw;
   a.pb = plan->bp_pb;
@@ -724,65 +780,111 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     a.pair_pad = pad - kb0;
   }
   for (int d = 0; d < 8; ++d) a.peer[d] = d < n_peer ? reinterpret_cast<float2*>(peers[d]) : nullptr;
-  a.ws = nullptr;
-  a.ws_plane = 0;
-  a.ws_planes = 0;
-  a.tile_count = nullptr;
   static const bool scatter_nosplit = [] {   // tuning switch: scatters always unsplit
     const char* e = getenv("SAR_BP_SCATTER_NOSPLIT");
     return e && e[0] == '1';
   }();
-  if (nchirp > 0 && !(n_peer > 0 && scatter_nosplit)) {
-    // a launch that would run chirp-split: one workspace plane per chunk (+ per-tile counters for
-    // a scatter, whose last chunk per tile publishes it) from the plan's pool; without them it
-    // runs unsplit
-    int k = 1;
-    sar::BpArgs q = a;   // the launcher's split of this launch (its scatter policy included)
-    q.split_query = &k;
-    if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, plan->near_field, (cudaStream_t)stream) == cudaSuccess &&
-        k > 1) {
-      a.ws_plane = (long)nrow * g.nx;
-      if (cudaMallocFromPoolAsync((void**)&a.ws, (size_t)k * a.ws_plane * sizeof(float2), plan->pool,
-                                  (cudaStream_t)stream) != cudaSuccess ||
-          (n_peer > 0 && cudaMallocFromPoolAsync((void**)&a.tile_count, (size_t)a.ntile * sizeof(int), plan->pool,
-                                                 (cudaStream_t)stream) != cudaSuccess)) {
-        cudaGetLastError();
-        if (a.ws) cudaFreeAsync(a.ws, (cudaStream_t)stream);
-        a.ws = nullptr;
-        a.tile_count = nullptr;
-      } else {
-        a.ws_planes = k;
+  // One launch per run of tiles: a plan with near-field tiles runs them (and only them) on the
+  // kernel with the per-tile SAFE branch; every other tile runs on the fast kernel.
+  std::vector<TileRun> runs = tile_runs(plan, tile0, ntile, tiles_x);
+  cudaError_t e = cudaSuccess;
+  int64_t launched = pairs ? 1 : 0;
+  // near-field runs next to far-field ones go to the plan's side stream (fork / join events), so
+  // the small near-field launch shares the GPU with the far-field one instead of following it
+  bool have_near = false, have_far = false;
+  for (const TileRun& run : runs) (run.near ? have_near : have_far) = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (have_near && have_far) {
+    std::lock_guard<std::mutex> lock(plan->side_mutex);
+    if (!plan->side && cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      plan->side = nullptr;
+    }
+    side = plan->side;
+  }
+  if (side && (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+               cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess ||
+               cudaEventRecord(fork, (cudaStream_t)stream) != cudaSuccess ||
+               cudaStreamWaitEvent(side, fork, 0) != cudaSuccess)) {
+    cudaGetLastError();
+    side = nullptr;   // serial fallback on the caller's stream
+  }
+  for (const TileRun& run : runs) {
+    void* const rstream = (side && run.near) ? (void*)side : (void*)stream;
+    sar::BpArgs b = a;
+    b.ty0 = run.tile0 / tiles_x;   // the launch covers whole tile rows; [tile_lo, tile_hi) compute
+    b.tile_lo = run.tile0 - b.ty0 * tiles_x;
+    b.tile_hi = b.tile_lo + run.ntile;
+    b.ntile = ((run.tile0 + run.ntile - 1) / tiles_x + 1) * tiles_x - b.ty0 * tiles_x;
+    b.ws = nullptr;
+    b.ws_plane = 0;
+    b.ws_planes = 0;
+    b.tile_count = nullptr;
+    // rows of this run inside the call's image rows (the chunk planes cover only those)
+    const int rr0 = std::max(0, b.ty0 * TYp - row0);
+    const int rr1 = std::min(nrow, (b.ty0 + b.ntile / tiles_x) * TYp - row0);
+    float2* ws_buf = nullptr;
+    if (nchirp > 0 && !(n_peer > 0 && scatter_nosplit)) {
+      // a launch that would run chirp-split: one workspace plane per chunk (+ per-tile counters
+      // for a scatter, whose last chunk per tile publishes it) from the plan's pool; without
+      // them it runs unsplit
+      int k = 1;
+      sar::BpArgs q = b;   // the launcher's split of this launch (its scatter policy included)
+      q.split_query = &k;
+      if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, run.near, (cudaStream_t)rstream) == cudaSuccess &&
+          k > 1) {
+        b.ws_plane = (long)(rr1 - rr0) * g.nx;
+        if (cudaMallocFromPoolAsync((void**)&ws_buf, (size_t)k * b.ws_plane * sizeof(float2), plan->pool,
+                                    (cudaStream_t)rstream) != cudaSuccess ||
+            (n_peer > 0 && cudaMallocFromPoolAsync((void**)&b.tile_count, (size_t)b.ntile * sizeof(int), plan->pool,
+                                                   (cudaStream_t)rstream) != cudaSuccess)) {
+          cudaGetLastError();
+          if (ws_buf) cudaFreeAsync(ws_buf, (cudaStream_t)rstream);
+          ws_buf = nullptr;
+          b.tile_count = nullptr;
+        } else {
+          // planes indexed by the image row (kernel and split sum): offset to the run's rows
+          b.ws = ws_buf - (ptrdiff_t)rr0 * g.nx;
+          b.ws_planes = k;
+        }
       }
     }
+    int ksplit = 1;
+    b.ksplit_out = &ksplit;
+    e = sar::launch_bp(b, bistatic, doppler_bins != nullptr, run.near, (cudaStream_t)rstream);
+    if (e == cudaSuccess) ++launched;
+    if (e == cudaSuccess && ksplit > 1 && n_peer == 0) {
+      // the chunk planes in chunk order into the image (deterministic)
+      sar::SplitSumArgs sa;
+      sa.img = b.img;
+      sa.ws = b.ws;
+      sa.plane = b.ws_plane;
+      sa.planes = ksplit;
+      sa.tile0 = run.tile0;
+      sa.ntile = run.ntile;
+      sa.tiles_x = tiles_x;
+      sa.tile_y = TYp;
+      sa.row0 = row0;
+      sa.nrow = nrow;
+      sa.nx = g.nx;
+      sa.accumulate = accumulate;
+      e = sar::launch_split_sum(sa, (cudaStream_t)rstream);
+      if (e == cudaSuccess) ++launched;
+    }
+    if (ws_buf) cudaFreeAsync(ws_buf, (cudaStream_t)rstream);
+    if (b.tile_count) cudaFreeAsync(b.tile_count, (cudaStream_t)rstream);
+    if (e != cudaSuccess) break;
   }
-  int ksplit = 1;
-  a.ksplit_out = &ksplit;
-  cudaError_t e = sar::launch_bp(a, bistatic, doppler_bins != nullptr, plan->near_field,
-                                 (cudaStream_t)stream);
-  bool summed = false;
-  if (e == cudaSuccess && ksplit > 1 && n_peer == 0) {
-    // the chunk planes in chunk order into the image (deterministic)
-    sar::SplitSumArgs sa;
-    sa.img = a.img;
-    sa.ws = a.ws;
-    sa.plane = a.ws_plane;
-    sa.planes = ksplit;
-    sa.tile0 = tile0;
-    sa.ntile = ntile;
-    sa.tiles_x = tiles_x;
-    sa.tile_y = TYp;
-    sa.row0 = row0;
-    sa.nrow = nrow;
-    sa.nx = g.nx;
-    sa.accumulate = accumulate;
-    e = sar::launch_split_sum(sa, (cudaStream_t)stream);
-    summed = true;
+  if (side) {
+    if (cudaEventRecord(join, side) == cudaSuccess) cudaStreamWaitEvent((cudaStream_t)stream, join, 0);
+    else cudaStreamSynchronize(side);
   }
-  if (a.ws) cudaFreeAsync(a.ws, (cudaStream_t)stream);
-  if (a.tile_count) cudaFreeAsync(a.tile_count, (cudaStream_t)stream);
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
   if (pairs) cudaFreeAsync(pairs, (cudaStream_t)stream);
+  plan->launches.fetch_add(launched);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
-  plan->launches.fetch_add((pairs ? 2 : 1) + (summed ? 1 : 0));
   return SAR_OK;
 }
 }  // namespace
