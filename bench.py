@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms per 8192-chirp 30×30 m BP image; pixel·chirp updates/s at 1/2/4/8 B200"
 UNIT = "px·chirp·rx updates/s"
+STREAM_METRIC = "ms per 8192-chirp streaming frame; image pixel·chirp updates/s"
 WORKLOADS = {
     "C3": "C3: 8192 chirps x 512 samples, 1 RX, curved non-equidistant track (R = 20 m, 6->9 m/s), "
           "30 m x 30 m grid at 1 cm (3000 x 3000 px), Fig.1-style scene + 96 isolated points, AWGN 0.05",
@@ -203,14 +204,17 @@ def run_reference(args):
     wall = sum(r["t_rc_s"] + r["t_bp_s"] for r in per_step) / len(per_step)
     sample = (f"per step: oracle range compression of all {scn.n_chirps * scn.n_rx} rows + oracle BP of "
               f"{per_step[0]['n_pix']} random pixels x {scn.n_chirps} chirps x {scn.n_rx} RX; "
-              f"full-image time extrapolated per pixel")
+              f"full-image time (ms_per_step) extrapolated per pixel from that sample")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "extrapolated": True, "sample_pixels": per_step[0]["n_pix"], "sample_fraction": per_step[0]["n_pix"] / scn.grid.nx / scn.grid.ny,
         "sample_wall_ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "config": args.config},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "config": config_dict(args, scn),
+        "parallelism": f"fp64 CPU oracle, {cores} host threads (rank 0)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "per_core": value / cores, "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -218,18 +222,44 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+def config_dict(args, scn):
+    """The workload of the line: identical in both arms (the driver compares them)."""
+    r = scn.radar
+    return {"workload": WORKLOADS[args.config], "config": args.config, "pixels": scn.grid.nx * scn.grid.ny,
+            "chirps": scn.n_chirps, "n_rx": scn.n_rx, "samples": r.n_samples, "fft_len": r.fft_len,
+            "updates": scn.updates, "l2": L2_NOTE}
+
+
+L2_NOTE = "256 MB buffer written between timed steps (outside the event span)"
+
+
+def gather_summary(world, legs, check):
+    """N > 1: both gather legs of the same run.  ``legs`` maps "fused" / "nccl" to
+    {"ms": per-step ms (max over ranks), "bp_ms": per-rank BP ms list, "collective_ms": per-rank
+    ms of the collective / barrier after the BP} or None when the leg did not run."""
+    out = {"world": world, "headline": None}
+    for name in ("fused", "nccl"):
+        leg = legs.get(name)
+        out[f"{name}_ms"] = None if leg is None else leg["ms"]
+        out[f"{name}_bp_ms_per_rank"] = None if leg is None else leg["bp_ms"]
+        out[f"{name}_collective_ms_per_rank"] = None if leg is None else leg["collective_ms"]
+        out[f"{name}_check"] = check.get(name)
+    ok = [n for n in ("fused", "nccl") if legs.get(n) is not None and (check.get(n) or {}).get("ok")]
+    if ok:
+        out["headline"] = min(ok, key=lambda n: legs[n]["ms"])
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2306_09784_b200 import sar
-    from paper_2306_09784_b200.dist import row_partition
+    from paper_2306_09784_b200.dist import gather_rows, tile_partition, tile_row_partition
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
@@ -238,24 +268,29 @@ def run_ours(args):
 
     scn, raw = _setup(args.config, dev)
     g = scn.grid
-    row0, nrow = row_partition(g.ny, world, rank)
     lo, hi = scn.antenna_box(1e-3)
     plan = sar.Plan(scn.radar, g, scn.n_chirps, scn.n_rx, (lo, hi), device=local)
+    tiles_x, tiles_y = plan.tiles
+    ty = plan.info.tile_y
+    # fused leg: a balanced block of absolute tiles per rank (+-1 tile); NCCL leg: whole tile rows
+    t0, nt = tile_partition(tiles_x * tiles_y, world, rank)
+    parts = [tile_row_partition(tiles_y, ty, g.ny, world, r) for r in range(world)]
+    row0, nrow = parts[rank]
     tx = torch.as_tensor(scn.tx, device=dev)
     rx = None if scn.rx is None else torch.as_tensor(scn.rx, device=dev).contiguous()
     wsar = torch.as_tensor(scn.wsar, device=dev)
     prof = plan.empty_profiles()
-    local_img = plan.empty_image(nrow)
-    full_img = torch.empty((g.ny, g.nx), dtype=torch.complex64, device=dev) if world > 1 else local_img
-    # N > 1: the image gather fused into the BP epilogue (NEXT-4, symmetric memory: P2P stores
-    # or one multimem.st per tile); --gather nccl keeps the separate all_gather
+    per = max(n for _, n in parts)
+    local_buf = plan.empty_image(per)   # a block of `per` rows: the NCCL leg gathers equal chunks
+    local_img = local_buf[:nrow]
+    full_img = torch.empty((per * world, g.nx), dtype=torch.complex64, device=dev) if world > 1 else local_img
     fused, fused_err = None, None
-    if world > 1 and args.gather in ("fused", "multicast"):
+    if world > 1 and args.gather in ("auto", "fused", "multicast"):
         from paper_2306_09784_b200.dist import FusedRowGather
 
         try:
             fused = FusedRowGather(g.ny, g.nx, dev, prefer_multicast=args.gather == "multicast")
-        except Exception as e:  # no symmetric memory on this system: report and use NCCL
+        except Exception as e:  # no symmetric memory on this system: the NCCL leg alone
             fused_err = repr(e)[:200]
     polar = plan.polar
     if polar:   # Measure E: the polar image is resampled onto the Cartesian C0 grid in the step
@@ -265,96 +300,129 @@ def run_ours(args):
         cart_img = torch.empty((cart.ny, cart.nx), dtype=torch.complex64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
-    def step():
+    def step_fused():
         plan.range_compress(raw, wsar, out=prof, stream=stream)
         ev[1].record(stream)
-        if fused is not None:
-            plan.backproject_scatter(prof, tx, fused.ptrs, rx, row0=row0, nrow=nrow, multicast=fused.multicast,
-                                     stream=stream)
-            ev[2].record(stream)
-            fused.barrier()
-        else:
-            plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
-            ev[2].record(stream)
-        if world > 1 and fused is None:
-            if g.ny % world == 0:
-                dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1),
-                                            torch.view_as_real(local_img).view(-1))
-            else:   # ragged row blocks: padded gather (dist.gather_rows)
-                from paper_2306_09784_b200.dist import gather_rows
-
-                full_img.copy_(gather_rows(local_img, g.ny))
+        plan.backproject_scatter_tiles(prof, tx, fused.ptrs, t0, nt, rx, multicast=fused.multicast, stream=stream)
+        ev[2].record(stream)
+        fused.barrier()
         if polar:
-            sar.polar_to_cartesian(g, fused.image if fused is not None else full_img, cart, out=cart_img,
-                                   stream=stream)
+            sar.polar_to_cartesian(g, fused.image, cart, out=cart_img, stream=stream)
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    for _ in range(args.warmup):
-        ev[0].record(stream)
-        step()
-        ev[3].record(stream)
-    torch.cuda.synchronize()
-
-    # ---------------- timed region: K steps, device events, L2 flushed between steps
-    step_ms, bp_ms, rc_ms = [], [], []
-    l0 = plan.launches
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            ev[0].record(stream)
-            step()
-            ev[3].record(stream)
-            ev[3].synchronize()
-            step_ms.append(ev[0].elapsed_time(ev[3]))
-            rc_ms.append(ev[0].elapsed_time(ev[1]))
-            bp_ms.append(ev[1].elapsed_time(ev[2]))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = plan.launches - l0
-    gather_check = None
-    if fused is not None:
-        # outside the timed region: the fused image must equal the NCCL gather of the rows up
-        # to the fp32 order of chirp-chunk sums (both launches may be chirp-split; their L2
-        # reductions land in any order)
+    def step_nccl():
+        plan.range_compress(raw, wsar, out=prof, stream=stream)
+        ev[1].record(stream)
         plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
-        from paper_2306_09784_b200.dist import gather_rows
+        ev[2].record(stream)
+        if world > 1:
+            # equal chunks of `per` rows (a short last tile-row block carries padding rows)
+            dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1), torch.view_as_real(local_buf).view(-1))
+        if polar:
+            sar.polar_to_cartesian(g, image_of_nccl(), cart, out=cart_img, stream=stream)
 
-        ref = gather_rows(local_img, g.ny)
+    def image_of_nccl():
+        if world == 1:
+            return full_img
+        if all(n == per for _, n in parts):
+            return full_img[: g.ny]
+        return torch.cat([full_img[r * per: r * per + n] for r, (_, n) in enumerate(parts)])
+
+    def timed(step):
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
-        rel = float((ref - fused.image).abs().max() / ref.abs().max().clamp_min(1e-30))
-        gather_check = {"equal": bool(torch.equal(ref, fused.image)), "max_rel_diff": rel, "ok": rel <= 1e-5}
-        if not gather_check["ok"]:
-            print(f"bench: fused gather differs from the NCCL gather (max rel {rel:.2e})", file=sys.stderr)
-    total_ms = sum(step_ms)
+        step_ms, bp_ms, rc_ms, coll_ms = [], [], [], []
+        l0 = plan.launches
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.zero_()
+                ev[0].record(stream)
+                step()
+                ev[3].record(stream)
+                ev[3].synchronize()
+                step_ms.append(ev[0].elapsed_time(ev[3]))
+                rc_ms.append(ev[0].elapsed_time(ev[1]))
+                bp_ms.append(ev[1].elapsed_time(ev[2]))
+                coll_ms.append(ev[2].elapsed_time(ev[3]))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        mine = torch.tensor([sum(step_ms), sum(bp_ms), sum(rc_ms), sum(coll_ms)], dtype=torch.float64, device=dev)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allr, mine)
+        else:
+            allr = [mine]
+        allr = torch.stack(allr).cpu() / args.steps
+        return {"ms": float(allr[:, 0].max()), "bp_ms": [float(x) for x in allr[:, 1]],
+                "rc_ms": [float(x) for x in allr[:, 2]], "collective_ms": [float(x) for x in allr[:, 3]],
+                "launches": plan.launches - l0, "clocks": clk.summary(), "bp_mine_ms": sum(bp_ms) / len(bp_ms)}
+
+    legs, check = {}, {}
+    if fused is not None:
+        legs["fused"] = timed(step_fused)
+    legs["nccl"] = timed(step_nccl)
+    # ---------------- outside the timed regions: every leg's image against this plan's 1-GPU image
+    # (every pixel is computed in its absolute tile: equal up to the fp32 order of chirp-chunk sums)
     if world > 1:
-        t = torch.tensor([total_ms, sum(bp_ms)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, bp_total_ms = float(t[0]), float(t[1])
+        ref = plan.backproject(prof, tx, rx, stream=stream)
+        torch.cuda.synchronize()
+        scale = ref.abs().max().clamp_min(1e-30)
+        imgs = {"nccl": image_of_nccl()}
+        if fused is not None:
+            imgs["fused"] = fused.image
+        for name, im in imgs.items():
+            rel = float((im - ref).abs().max() / scale)
+            check[name] = {"max_rel_diff_to_1gpu_image": rel, "equal": bool(torch.equal(im, ref)), "ok": rel <= 1e-6}
+        flags = torch.tensor([0 if c["ok"] else 1 for c in check.values()], device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)   # every rank agrees on the verdict
+        for name, bad in zip(check, flags.tolist()):
+            check[name]["ok"] = check[name]["ok"] and not bad
+        del ref
     else:
-        bp_total_ms = sum(bp_ms)
-    ms_per_step = total_ms / args.steps
+        check["nccl"] = {"ok": True}
+    gather = gather_summary(world, legs, check) if world > 1 else None
+    head = "nccl" if world == 1 else gather["headline"]
+    if head is None:   # no leg produced the 1-GPU image: report the failure, no number
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "invalid":
+                              "no gather leg reproduced the 1-GPU image", "gather": gather,
+                              "config": config_dict(args, scn)}), flush=True)
+        plan.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return 1
+    leg = legs[head]
+    ms_per_step = leg["ms"]
     value = scn.updates / (ms_per_step * 1e-3)
 
-    # ---------------- roofline of the dominant kernel (bp_kernel)
+    # ---------------- roofline of the dominant kernel (bp_kernel), this rank's launches
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks = _peaks()
-    max_mhz = float(peaks.get("sm_max_mhz", clk.max_mhz or 1965.0))
-    bp_upd = nrow * g.nx * scn.n_chirps * scn.n_rx
-    bp_avg_s = (sum(bp_ms) / len(bp_ms)) * 1e-3
+    clocks = leg["clocks"]
+    max_mhz = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
+    if head == "fused":
+        # pixels of the rank's tiles (ragged last tile column / row clipped to the grid)
+        ntx = [min(32, g.nx - 32 * (t % tiles_x)) for t in range(t0, t0 + nt)]
+        nty = [min(ty, g.ny - ty * (t // tiles_x)) for t in range(t0, t0 + nt)]
+        bp_px = sum(a * b for a, b in zip(ntx, nty))
+    else:
+        bp_px = nrow * g.nx
+    bp_upd = bp_px * scn.n_chirps * scn.n_rx
+    bp_avg_s = leg["bp_mine_ms"] * 1e-3
     achieved = bp_upd / bp_avg_s
     peak = _alu_peak_upd_s(n_sm, max_mhz)
-    clocks = clk.summary()
     roofline = {
         "bound": "alu", "achieved": achieved, "peak": peak, "unit": "upd/s", "frac": achieved / peak,
         "traffic": _traffic_from_profiles(args.config),
         "kernel": "bp_kernel", "peak_basis": f"SFU: {n_sm} SM x 16 MUFU/clk x {max_mhz:.0f} MHz / 3 MUFU per update",
         "frac_at_measured_clock": (achieved / _alu_peak_upd_s(n_sm, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
-        "bp_ms": bp_avg_s * 1e3, "rc_ms": sum(rc_ms) / len(rc_ms),
+        "bp_ms": bp_avg_s * 1e3, "rc_ms": leg["rc_ms"][rank],
     }
 
     # ---------------- end to end through the C ABI with host buffers (sar_form_image)
@@ -408,38 +476,42 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = _oracle_sample(scn, raw.cpu().numpy(), target_s=args.cpu_s)
         cpu = {"value": res["value"], "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "per_core": res["value"] / (os.cpu_count() or 1),
                "sample": f"oracle range compression of all {scn.n_chirps * scn.n_rx} rows "
                          f"({res['t_rc_s']:.2f} s) + oracle BP of {res['n_pix']} random pixels x all chirps "
                          f"({res['t_bp_s']:.2f} s), full image extrapolated to {res['est_image_s']:.1f} s"}
 
     if rank == 0:
+        if world == 1:
+            par, step_txt = "pixel tiles x1", "sar_range_compress(all chirps) + sar_backproject(all rows)"
+        elif head == "fused":
+            par = (f"pixel tiles x{world} (balanced tile blocks) + gather fused into the BP epilogue "
+                   f"({'multimem.st' if fused.multicast else 'P2P stores'}, symmetric memory)")
+            step_txt = ("sar_range_compress(all chirps) + sar_backproject_scatter_tiles(rank tiles -> every "
+                        "rank's image) + symmetric-memory barrier")
+        else:
+            par = f"pixel tiles x{world} (blocks of whole tile rows) + NCCL all_gather_into_tensor"
+            step_txt = "sar_range_compress(all chirps) + sar_backproject(rank tile rows) + all_gather_into_tensor"
+        if polar:
+            step_txt += " + sar_polar_to_cartesian"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": (value / PAPER_UPD_S[args.config][0]) if args.config in PAPER_UPD_S else None,
             "baseline_note": PAPER_UPD_S[args.config][1] if args.config in PAPER_UPD_S else None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "config": args.config, "pixels": g.nx * g.ny,
-                       "chirps": scn.n_chirps, "n_rx": scn.n_rx, "samples": scn.radar.n_samples,
-                       "fft_len": scn.radar.fft_len, "n_bins": plan.n_bins, "updates": scn.updates,
-                       "parallelism": f"pixel rows x{world}" + (
-                           "" if world == 1 else
-                           (f" + gather fused into the BP epilogue ({'multimem.st' if fused.multicast else 'P2P stores'},"
-                            f" symmetric memory)" if fused is not None else " + NCCL all_gather")),
-                       "gather_check": gather_check, "fused_gather_error": fused_err,
-                       "l2": "256 MB buffer written between timed steps (outside the event span)",
-                       "step": "sar_range_compress(all chirps) + "
-                               + ("sar_backproject_scatter(rank rows -> every rank's image) + barrier" if fused is not None
-                                  else "sar_backproject(rank rows)" + (" + all_gather_into_tensor" if world > 1 else ""))
-                               + (" + sar_polar_to_cartesian" if polar else "")},
+            "config": config_dict(args, scn),
+            "parallelism": par, "step": step_txt, "n_bins": plan.n_bins,
+            "gather": gather, "fused_gather_error": fused_err,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": scn.updates / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_image": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "load_ms": load_ms, "load_note": "pinned H2D of raw samples + poses alone (Table 2 'Load')",
                     "api": "sar_form_image (C ABI, pinned host buffers: H2D raw+poses, rc, bp whose epilogue "
-                           "stores the image rows into the mapped pinned host buffer)"},
-            "gpu_launches": launches,
+                           "stores the image rows into the mapped pinned host buffer)"
+                           + ("" if world == 1 else "; each rank its tile-row block")},
+            "gpu_launches": leg["launches"],
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -560,7 +632,7 @@ def run_stream(args):
         step = "one frame: sar_range_compress + sar_backproject of this rank's chirps (+ reduce)"
     if rank == 0:
         print(json.dumps({
-            "metric": "ms per 8192-chirp streaming frame; image pixel·chirp updates/s",
+            "metric": STREAM_METRIC,
             "value": upd / (ms_frame * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_frame, "max_frame_ms": float(tot[1]),
             "realtime_budget_ms": 1024 * scn.radar.pri_s * 1e3, "higher_is_better": True,
@@ -590,17 +662,54 @@ def main(argv=None):
     ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--gather", default="fused", choices=["fused", "multicast", "nccl"],
-                    help="N > 1: image gather fused into the BP epilogue (symmetric memory; P2P stores, or "
-                         "multimem.st to the NVSwitch multicast address) or a separate NCCL all_gather")
+    ap.add_argument("--gather", default="auto", choices=["auto", "fused", "multicast", "nccl"],
+                    help="N > 1, image configs: besides the NCCL all_gather leg (always timed), time the gather "
+                         "fused into the BP epilogue (auto/fused: P2P stores, multicast: multimem.st to the "
+                         "NVSwitch multicast address; symmetric memory); nccl: the NCCL leg only.  C5: the "
+                         "chirp-shard reduction is an NCCL reduce unless fused/multicast (P2P red.add)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         if args.config in ("C5", "C5i"):
             raise SystemExit("--impl reference supports the image configs (C0-C4)")
-        return run_reference(args)
+        return run_reference(args)   # rank 0 alone (any launch); other ranks exit 0
+    world = _env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        if "WORLD_SIZE" in os.environ or args.gpus < 1:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+        return self_launch(args, argv)
     return run_stream(args) if args.config in ("C5", "C5i") else run_ours(args)
+
+
+def self_launch(args, argv):
+    """``bench.py --gpus N`` outside torchrun: start N ranks (one per GPU) with torchrun on this
+    node; rank 0's JSON line is the output.  With fewer than N GPUs visible, one JSON line says so
+    (no ranks sharing a GPU: their numbers would not be N-GPU numbers)."""
+    import socket
+    import subprocess
+
+    try:
+        import torch
+
+        ngpu = torch.cuda.device_count()
+    except Exception:
+        ngpu = 0
+    if ngpu < args.gpus:
+        legs = {"fused": None, "nccl": None}
+        print(json.dumps({"metric": METRIC if args.config not in ("C5", "C5i") else STREAM_METRIC, "value": None,
+                          "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "unavailable": f"--gpus {args.gpus}: {ngpu} GPU(s) visible",
+                          "gather": gather_summary(args.gpus, legs, {})}), flush=True)
+        return 0
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    argv = list(sys.argv[1:] if argv is None else argv)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -36,13 +36,41 @@ _lib = None
 C_LIGHT = 299792458.0
 
 
+_STAMP = _LIB + ".cpu"
+
+
+def _cpu_id() -> str:
+    """The host CPU the library was tuned for (-march=native): model name + flags."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            txt = f.read()
+        model = next((l.split(":", 1)[1].strip() for l in txt.splitlines() if l.startswith("model name")), "")
+        flags = next((l.split(":", 1)[1].strip() for l in txt.splitlines() if l.startswith("flags")), "")
+        return model + "|" + flags
+    except OSError:
+        return "unknown"
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle/sar_oracle.c -> oracle/liboracle.so with gcc (no GPU needed)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile oracle/sar_oracle.c -> oracle/liboracle.so with gcc (no GPU needed): -O3
+    -march=native as BASELINE.md's CPU-baseline plan states, FMA contraction off (the
+    arithmetic stays the source's, operation by operation).  A library built for another
+    host CPU (the tree travels to the GPU box) is rebuilt there."""
+    stale = not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
+    if not stale:
+        try:
+            with open(_STAMP) as f:
+                stale = f.read() != _cpu_id()
+        except OSError:
+            stale = True
+    if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
-        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm", "-lpthread"]
+        cmd = ["gcc", "-O3", "-march=native", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared", "-o", tmp, _SRC,
+               "-lm", "-lpthread"]
         subprocess.check_call(cmd)
         os.replace(tmp, _LIB)
+        with open(_STAMP, "w") as f:
+            f.write(_cpu_id())
     return _LIB
 
 

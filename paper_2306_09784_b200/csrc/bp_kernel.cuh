@@ -723,10 +723,11 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           } else {
             for (int q = 0; q < a.n_peer; ++q) a.peer[q][o] = make_float2(acc_r[p], acc_i[p]);
           }
-        } else if (a.ksplit > 1) {
-          // chirp chunks: each stores its partial into its own workspace plane; the split-sum
-          // kernel adds the planes in chunk order (deterministic, unlike reductions)
-          __stcg(a.ws + (size_t)chunk_e * a.ws_plane + (size_t)gy[p] * a.nx + gx[p], make_float2(acc_r[p], acc_i[p]));
+        } else if (a.ksplit > 1 && chunk_e > 0) {
+          // chirp chunks 1.. store their partials into workspace planes 0..; chunk 0 stores (or
+          // accumulates) into the image like an unsplit launch, and the split-sum kernel then
+          // adds the planes in chunk order (deterministic, unlike reductions)
+          __stcg(a.ws + (size_t)(chunk_e - 1) * a.ws_plane + (size_t)gy[p] * a.nx + gx[p], make_float2(acc_r[p], acc_i[p]));
         } else if (a.accumulate) {
           const float2 o = *dst;
           *dst = make_float2(o.x + acc_r[p], o.y + acc_i[p]);
@@ -835,7 +836,9 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
     return cudaSuccess;
   }
   // a split needs its workspace planes (and tile counters for a scatter); without them, unsplit
-  if (b.ksplit > 1 && (!a.ws || a.ws_planes < b.ksplit || (a.n_peer > 0 && !a.tile_count))) split(1);
+  // (a plain launch keeps chunk 0 in the image: ksplit - 1 planes; a scatter needs ksplit)
+  if (b.ksplit > 1 && (!a.ws || a.ws_planes < b.ksplit - (a.n_peer > 0 ? 0 : 1) || (a.n_peer > 0 && !a.tile_count)))
+    split(1);
   if (b.ksplit > 1 && a.n_peer > 0) {
     cudaError_t e = cudaMemsetAsync(a.tile_count, 0, sizeof(int) * (size_t)a.ntile, s);
     if (e != cudaSuccess) return e;

@@ -104,13 +104,14 @@ struct DopArgs {
 };
 cudaError_t launch_doppler(const DopArgs& a, cudaStream_t s);
 cudaError_t launch_sum(float2* out, const float2* in, int n, long stride, long count, cudaStream_t s);
-// Chirp-split sum: img[p] (+)= ws[0][p] + ws[1][p] + ... (chunk order) for the pixels of the
-// absolute tiles [tile0, tile0 + ntile) inside rows [row0, row0 + nrow) (img, ws at row row0).
+// Chirp-split sum: img[p] = ((img[p] + ws[0][p]) + ws[1][p]) + ... (chunk order; img holds chunk
+// 0) for the pixels of the absolute tiles [tile0, tile0 + ntile) inside rows [row0, row0 + nrow)
+// (img, ws at row row0).
 struct SplitSumArgs {
   float2* img;
   const float2* ws;
   long plane;
-  int planes, tile0, ntile, tiles_x, tile_y, row0, nrow, nx, accumulate;
+  int planes, tile0, ntile, tiles_x, tile_y, row0, nrow, nx;
 };
 cudaError_t launch_split_sum(const SplitSumArgs& a, cudaStream_t s);
 

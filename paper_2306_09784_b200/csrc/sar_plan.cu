@@ -835,7 +835,8 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
       if (sar::launch_bp(q, bistatic, doppler_bins != nullptr, run.near, (cudaStream_t)rstream) == cudaSuccess &&
           k > 1) {
         b.ws_plane = (long)(rr1 - rr0) * g.nx;
-        if (cudaMallocFromPoolAsync((void**)&ws_buf, (size_t)k * b.ws_plane * sizeof(float2), plan->pool,
+        const int planes = n_peer > 0 ? k : k - 1;   // a plain launch keeps chunk 0 in the image
+        if (cudaMallocFromPoolAsync((void**)&ws_buf, (size_t)planes * b.ws_plane * sizeof(float2), plan->pool,
                                     (cudaStream_t)rstream) != cudaSuccess ||
             (n_peer > 0 && cudaMallocFromPoolAsync((void**)&b.tile_count, (size_t)b.ntile * sizeof(int), plan->pool,
                                                    (cudaStream_t)rstream) != cudaSuccess)) {
@@ -846,7 +847,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
         } else {
           // planes indexed by the image row (kernel and split sum): offset to the run's rows
           b.ws = ws_buf - (ptrdiff_t)rr0 * g.nx;
-          b.ws_planes = k;
+          b.ws_planes = planes;
         }
       }
     }
@@ -860,7 +861,7 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
       sa.img = b.img;
       sa.ws = b.ws;
       sa.plane = b.ws_plane;
-      sa.planes = ksplit;
+      sa.planes = ksplit - 1;
       sa.tile0 = run.tile0;
       sa.ntile = run.ntile;
       sa.tiles_x = tiles_x;
@@ -868,7 +869,6 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
       sa.row0 = row0;
       sa.nrow = nrow;
       sa.nx = g.nx;
-      sa.accumulate = accumulate;
       e = sar::launch_split_sum(sa, (cudaStream_t)rstream);
       if (e == cudaSuccess) ++launched;
     }

@@ -38,8 +38,8 @@ __global__ void sum_kernel(float2* __restrict__ out, const float2* __restrict__ 
   }
 }
 
-// Chirp-split sum, one CTA per tile of the launch: pixel (x, y) of the tile gets
-// ws[0] + ws[1] + ... in chunk order (+ the image's own value first when accumulating).  Rows of a
+// Chirp-split sum, one CTA per tile of the launch: pixel (x, y) of the tile (holding chunk 0's
+// store, or its accumulation) gets + ws[0] + ws[1] + ... in chunk order.  Rows of a
 // tile are 32 contiguous pixels (256 B), so each warp reads and writes whole rows.
 __global__ void __launch_bounds__(256) split_sum_kernel(const SplitSumArgs a) {
   const int tile = a.tile0 + blockIdx.x;
@@ -50,16 +50,11 @@ __global__ void __launch_bounds__(256) split_sum_kernel(const SplitSumArgs a) {
     const int y = J0 + yl - a.row0;
     if (y < 0 || y >= a.nrow) continue;
     const size_t o = (size_t)y * a.nx + x;
-    float2 s = __ldcs(a.ws + o);
-    for (int c = 1; c < a.planes; ++c) {
+    float2 s = a.img[o];
+    for (int c = 0; c < a.planes; ++c) {
       const float2 v = __ldcs(a.ws + (size_t)c * a.plane + o);
       s.x += v.x;
       s.y += v.y;
-    }
-    if (a.accumulate) {
-      const float2 v = a.img[o];
-      s.x = v.x + s.x;
-      s.y = v.y + s.y;
     }
     a.img[o] = s;
   }

@@ -75,3 +75,25 @@ def sample_indices(scn, gpu_abs=None, stride=(97, 101), win=3, top=32):
         pts.append(w[ok])
     allp = np.concatenate(pts)
     return np.unique(allp, axis=0)
+
+
+def c6_indices(scn, gpu_abs, stride=31, win=24, top=32):
+    """The C-6 protocol: WHOLE grid rows and columns at ``stride`` (coprime with the
+    32-px tile, so every tile row / column offset is visited), the last (ragged) row and column,
+    and +-``win`` px windows around every isolated target and the GPU's ``top`` largest pixels.
+    Returns unique (j, i) pairs."""
+    g = scn.grid
+    rows = np.unique(np.r_[np.arange(0, g.ny, stride), g.ny - 1])
+    cols = np.unique(np.r_[np.arange(0, g.nx, stride), g.nx - 1])
+    pts = [np.stack(np.meshgrid(rows, np.arange(g.nx), indexing="ij"), -1).reshape(-1, 2),
+           np.stack(np.meshgrid(np.arange(g.ny), cols, indexing="ij"), -1).reshape(-1, 2)]
+    centres = [tuple(c) for c in scn.isolated]
+    flat = np.argsort(gpu_abs.reshape(-1))[::-1][:top]
+    centres += [tuple(np.unravel_index(f, gpu_abs.shape)) for f in flat]
+    d = np.arange(-win, win + 1)
+    for (j, i) in centres:
+        jj, ii = np.meshgrid(j + d, i + d, indexing="ij")
+        w = np.stack([jj, ii], -1).reshape(-1, 2)
+        ok = (w[:, 0] >= 0) & (w[:, 0] < g.ny) & (w[:, 1] >= 0) & (w[:, 1] < g.nx)
+        pts.append(w[ok])
+    return np.unique(np.concatenate(pts), axis=0)

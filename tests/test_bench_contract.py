@@ -26,7 +26,8 @@ def test_reference_arm_json_line():
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 1
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["higher_is_better"] is True
-    assert "workload" in d["config"]
+    assert "workload" in d["config"] and d["config"]["config"] == "C3"
+    assert d["extrapolated"] is True and 0 < d["sample_fraction"] < 1
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
     e = d["e2e"]
@@ -47,3 +48,28 @@ def test_our_arm_json_line():
     assert d["gpu_launches"] >= 3 * d["steps"]
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and isinstance(c["reasons"], list)
+
+
+def test_multi_gpu_line_without_enough_gpus():
+    """``--gpus 2`` outside torchrun takes the self-launch path; with fewer GPUs visible (this CPU
+    box: none) it prints one JSON line saying so, carrying both gather legs' keys."""
+    d = _run(["--gpus", "2", "--steps", "1", "--warmup", "3"], 300)
+    assert d["n_gpus"] == 2 and d["value"] is None and "unavailable" in d
+    g = d["gather"]
+    for k in ("fused_ms", "nccl_ms", "fused_bp_ms_per_rank", "nccl_bp_ms_per_rank", "fused_collective_ms_per_rank",
+              "nccl_collective_ms_per_rank", "headline"):
+        assert k in g
+
+
+def test_gather_summary_picks_the_fastest_verified_leg():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    legs = {"fused": {"ms": 7.7, "bp_ms": [7.6, 7.5], "collective_ms": [0.05, 0.1]},
+            "nccl": {"ms": 8.0, "bp_ms": [7.6, 7.6], "collective_ms": [0.3, 0.3]}}
+    g = bench.gather_summary(2, legs, {"fused": {"ok": True}, "nccl": {"ok": True}})
+    assert g["headline"] == "fused" and g["fused_ms"] == 7.7 and g["nccl_ms"] == 8.0
+    g = bench.gather_summary(2, legs, {"fused": {"ok": False}, "nccl": {"ok": True}})
+    assert g["headline"] == "nccl"
+    g = bench.gather_summary(2, {"fused": None, "nccl": legs["nccl"]}, {"nccl": {"ok": False}})
+    assert g["headline"] is None and g["fused_ms"] is None

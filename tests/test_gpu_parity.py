@@ -8,7 +8,7 @@ import oracle
 import sarsim
 from sarsim import C_LIGHT, Grid, Scenario
 
-from .helpers import REL_TOL, gpu_image, oracle_image, oracle_profiles, rel_err, sample_indices
+from .helpers import REL_TOL, c6_indices, gpu_image, oracle_image, oracle_profiles, rel_err, sample_indices
 
 pytestmark = pytest.mark.gpu
 
@@ -454,7 +454,7 @@ def test_C5_streaming_frame_sampled_parity_and_chirp_shards(cuda_lib):
 
 def test_incremental_streaming_equals_one_shot_frame(cuda_lib):
     """NEXT-2: with a world-fixed grid the frame after hop h is the sum of the last 8 per-hop
-    partial images; it equals one back-projection of the same 8192 chirps."""
+    partial images; it equals one back-projection of the same 8192 chirps, and the oracle's."""
     import torch
 
     from paper_2306_09784_b200.stream import IncrementalStream
@@ -471,7 +471,19 @@ def test_incremental_streaming_equals_one_shot_frame(cuda_lib):
     prof = ref_plan.range_compress(raw)
     one = ref_plan.backproject(prof, tx, chirp0=3 * 1024, nchirp=8 * 1024)
     torch.cuda.synchronize()
-    assert rel_err(frame.cpu().numpy(), one.cpu().numpy()) < 1e-5
+    f = frame.cpu().numpy()
+    assert rel_err(f, one.cpu().numpy()) < 1e-5
+    # the streamed frame against the oracle's BP of the frame's 8192 chirps (continuous
+    # processing), on the C-6 sample of the world-fixed grid
+    c0 = 3 * 1024
+    sub = sarsim.Scenario("C5i-frame", scn.radar, scn.grid, scn.tx[c0:c0 + 8192], None, scn.targets, scn.amps,
+                          np.zeros((0, 2), int), scn.wsar[c0:c0 + 8192])
+    idx = c6_indices(sub, np.abs(f), stride=31, win=24)
+    ref_prof = oracle_profiles(sub, raw[c0:c0 + 8192].cpu().numpy(), ref_plan.k_lo, ref_plan.n_bins)
+    ref = oracle.backproject(ref_prof, ref_plan.k_lo, scn.radar, sub.tx, None, scn.grid.pixel_list(idx))
+    got = f[idx[:, 0], idx[:, 1]]
+    assert rel_err(got, ref) <= REL_TOL
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
     st.close()
     ref_plan.close()
 
@@ -489,17 +501,25 @@ def test_image_sum_kernel(cuda_lib):
 
 
 # ----------------------------------------------------------------------------- full-size configs
+# C-6 sample per config: (stride of whole rows / columns, window half-width); C4 (36 Mpx x 4 RX) is
+# thinned to keep its oracle leg near a minute on 16 host cores
+C6_PROTOCOL = {"C2": (31, 24), "C3": (31, 24), "C0": (31, 24), "C6": (31, 24), "C4": (191, 12)}
+
+
 @pytest.mark.parametrize("cfg", ["C2", "C3", "C0", "C4", "C6"])
 def test_full_size_config_sampled_parity(cuda_lib, cfg):
-    """BASELINE configs at full size in the bench's launch configuration; the oracle on the
-    C-6 sample (strided rows/cols + windows around isolated targets and GPU maxima)."""
+    """BASELINE configs at full size in the bench's launch configuration, against the oracle on
+    the C-6 protocol sample: whole rows and columns at a stride coprime with the 32-px tile (every
+    tile offset, the ragged last tile row and column included), +-24 px windows around every
+    isolated target and the GPU's 32 largest pixels (C3: ~0.85 M px x 8192 chirps)."""
     scn = sarsim.make_config(cfg)
     raw = _raw(scn)
     img, prof, plan = gpu_image(scn, raw, return_prof=True)
     a = np.abs(img.cpu().numpy())
     g = scn.grid
-    stride = {"C2": (97, 101), "C3": (149, 151), "C0": (61, 67), "C4": (397, 401), "C6": (61, 67)}[cfg]
-    idx = sample_indices(scn, a, stride=stride, win=2 if cfg == "C4" else 3)
+    stride, win = C6_PROTOCOL[cfg]
+    idx = c6_indices(scn, a, stride=stride, win=win)
+    assert np.any(idx[:, 0] == g.ny - 1) and np.any(idx[:, 1] == g.nx - 1)
     pix = g.pixel_list(idx)
     # oracle on the crop the plan keeps (it raises if any pixel needed a bin outside it)
     ref_prof = oracle_profiles(scn, raw.cpu().numpy(), plan.k_lo, plan.n_bins)
@@ -520,6 +540,20 @@ def test_full_size_config_sampled_parity(cuda_lib, cfg):
         r = np.sort(np.abs(ref[sel]))
         if r[-1] > (1 + 4e-3) * r[-2]:
             assert np.argmax(np.abs(got[sel])) == np.argmax(np.abs(ref[sel]))
+
+
+def test_zero_input_gives_zero_image(cuda_lib):
+    """T9 on the GPU: zero raw samples give exactly zero profiles and a zero image (monostatic and
+    bistatic, unsplit and chirp-split launches)."""
+    import torch
+
+    for n_rx, nchirp in ((1, 100), (3, 2048)):
+        scn = sarsim.small_config(n_chirps=nchirp, ns=128, nx=40, ny=33, seed=61, n_rx=n_rx)
+        raw = torch.zeros((nchirp, n_rx, 128), dtype=torch.float32, device="cuda:0")
+        img, prof, plan = gpu_image(scn, raw, return_prof=True)
+        torch.cuda.synchronize()
+        assert torch.count_nonzero(prof) == 0 and torch.count_nonzero(img) == 0
+        plan.close()
 
 
 @pytest.mark.parametrize("shape", ["4,4", "4,8", "8,8", "8,4,2,8", "8,4,5,4"])
