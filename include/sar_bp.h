@@ -92,7 +92,9 @@ typedef struct {
 /* Declared axis-aligned bounding box of ALL antenna phase centres (TX and RX)
  * the plan will be used with.  The range crop is derived from it and the grid box
  * with the triangle inequality; positions outside it give wrong values (never an
- * out-of-bounds access).  sar_form_image verifies its host positions against it. */
+ * out-of-bounds access: pair-row copies are clamped into their row, and a polar plan's
+ * tighter window bound is backed by guard entries up to the triangle bound, which holds
+ * for any position).  sar_form_image verifies its host positions against it. */
 typedef struct {
   double lo[3], hi[3];
 } sar_box_t;
@@ -174,7 +176,8 @@ sar_status_t sar_range_compress(sar_plan_t plan, const float* raw, const float* 
  *                         monostatic q_rx = q_tx (then n_rx must be 1)
  *   doppler_bins dev float [ny][nx] per-pixel f_doppler in bins (Measure D,
  *                         P:L311-317) or NULL (no Doppler term, A10); requires
- *                         doppler_max_bins >= max |doppler_bins| in the plan
+ *                         doppler_max_bins >= max |doppler_bins| in the plan (values
+ *                         beyond it are clamped to +-doppler_max_bins)
  *   image     dev complex [nrow][nx]: row r holds grid row row0 + r
  *   accumulate 0: image = P;  1: image += P (chirp sharding, NCCL reduce)
  * nrow == 0 is a no-op; nchirp == 0 writes zeros (accumulate = 0) or nothing.

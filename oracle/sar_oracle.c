@@ -342,7 +342,8 @@ int oracle_doppler_table(double f0_hz, double fs_hz, int nfft, const double* pix
  * A18): for Cartesian pixel (x0 + ix dx, y0 + iy dy) take its polar coordinates about
  * (xc, yc), r = |(x - xc, y - yc)|, th = atan2(x - xc, y - yc) (bearing from +y toward
  * +x), and interpolate the polar image bilinearly in the fractional indices
- * ((th - th0) / dth, (r - r0) / dr); pixels outside [0, n_th - 1] x [0, n_r - 1] are 0.
+ * ((th - th0) / dth, (r - r0) / dr), the bearing difference taken modulo 2 pi about the
+ * sector centre; pixels outside [0, n_th - 1] x [0, n_r - 1] (up to 1e-9 of an index) are 0.
  *   in  [n_r][n_th][2] (re, im);  out [ny][nx][2]. */
 int oracle_polar_to_cartesian(double xc, double yc, double r0, double dr, double th0, double dth,
                               int n_th, int n_r, const double* in, double x0, double y0, double dx,
@@ -351,10 +352,18 @@ int oracle_polar_to_cartesian(double xc, double yc, double r0, double dr, double
   for (int iy = 0; iy < ny; ++iy) {
     for (int ix = 0; ix < nx; ++ix) {
       const double px = x0 + ix * dx - xc, py = y0 + iy * dy - yc;
-      const double fi = (atan2(px, py) - th0) / dth;
-      const double fj = (sqrt(px * px + py * py) - r0) / dr;
+      /* bearing relative to the sector centre, wrapped into [-pi, pi): bearings are angles
+       * (A19), so a sector may cross +-pi and th0 may be given in any period */
+      const double half = 0.5 * (n_th - 1) * dth;
+      double dbear = atan2(px, py) - (th0 + half);
+      dbear -= 2.0 * ORACLE_PI * floor((dbear + ORACLE_PI) / (2.0 * ORACLE_PI));
+      double fi = (dbear + half) / dth;
+      double fj = (sqrt(px * px + py * py) - r0) / dr;
       double re = 0.0, im = 0.0;
-      if (fi >= 0.0 && fj >= 0.0 && fi <= n_th - 1 && fj <= n_r - 1) {
+      /* nodes on the sector boundary are inside (1e-9 of an index of rounding slack) */
+      if (fi >= -1e-9 && fj >= -1e-9 && fi <= n_th - 1 + 1e-9 && fj <= n_r - 1 + 1e-9) {
+        fi = fi < 0.0 ? 0.0 : (fi > n_th - 1 ? n_th - 1 : fi);
+        fj = fj < 0.0 ? 0.0 : (fj > n_r - 1 ? n_r - 1 : fj);
         int i0 = (int)floor(fi), j0 = (int)floor(fj);
         if (i0 > n_th - 1) i0 = n_th - 1;
         if (j0 > n_r - 1) j0 = n_r - 1;

@@ -10,8 +10,8 @@ bool bp_shape_supported(int ncw, int pb) {
   return (ncw == 8 && pb == 4) || (ncw == 4 && pb == 8) || (ncw == 4 && pb == 4) || (ncw == 8 && pb == 8);
 }
 
-size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic) {
-  return make_layout(W, CB, n_rx, S, bistatic).total;
+size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic, int guard) {
+  return make_layout(W, CB, n_rx, S, bistatic, guard).total;
 }
 
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {
@@ -27,5 +27,16 @@ cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, c
 extern "C" int sar_debug_trace(void* dst, void* dst_wid) {
   cudaMemcpyFromSymbol(dst, sar::g_trace, sizeof(sar::g_trace));
   return (int)cudaMemcpyFromSymbol(dst_wid, sar::g_trace_wid, sizeof(sar::g_trace_wid));
+}
+#endif
+
+#ifdef SAR_DEBUG_CHECKS
+extern "C" int sar_debug_violations_plain(unsigned long long* out4, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out4, sar::g_violations, sizeof(sar::g_violations));
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(sar::g_violations, z, sizeof(z));
+  }
+  return (int)e;
 }
 #endif

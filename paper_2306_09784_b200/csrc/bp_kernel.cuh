@@ -116,6 +116,18 @@ __device__ __forceinline__ void tr_ids(int trc, int w) {
 #define SAR_TR(w, it, k)
 #endif
 
+#ifdef SAR_DEBUG_CHECKS
+// bounds-check build (tools/check_cases.py): violations counted per kind, read back through
+// sar_debug_violations_*: [0] consumer window index outside its item's W entries, [1] chirp-chunk
+// workspace plane out of range, [2] pair-row bulk copy outside its row (clamped), [3] consumer
+// read outside the shared-memory allocation
+__device__ unsigned long long g_violations[4];
+#define SAR_CHECK(cond, k) \
+  if (!(cond)) atomicAdd(&g_violations[k], 1ull)
+#else
+#define SAR_CHECK(cond, k)
+#endif
+
 __device__ __forceinline__ unsigned ctaid_x() {   // opaque to CSE: not kept live across loops
   unsigned v;
   asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v));
@@ -227,15 +239,19 @@ struct Layout {
   uint32_t rec, kwin, win, total;
 };
 
-__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic) {
+//   guard: G spare entries before the first and after the last window (polar plans): a consumer
+//          index past its item's window (an antenna outside the declared box breaks the polar
+//          window bound, never the triangle bound the guard covers) reads wrong values, never
+//          outside the allocation
+__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic, int guard) {
   Layout L;
   L.items = CB * n_rx;
   L.legs = bistatic ? CB + L.items : L.items;
   L.rec = 16 * kBpMaxStages;
   L.kwin = L.rec + (uint32_t)S * L.legs * 32;
   const uint32_t kw_bytes = ((uint32_t)S * L.items * 8 + 15u) & ~15u;
-  L.win = L.kwin + kw_bytes;
-  L.total = L.win + (uint32_t)S * L.items * W * 16;
+  L.win = L.kwin + kw_bytes + 16u * (uint32_t)guard;
+  L.total = L.win + (uint32_t)S * L.items * W * 16 + 16u * (uint32_t)guard;
   return L;
 }
 
@@ -247,7 +263,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
   const int S = a.S;
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC);
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC, a.guard);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpMaxStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -376,6 +392,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         const uint32_t wdst = smem_u32(swin);
         for (int e = lane; e < items; e += 32) {
           const int2 kw = skw[e];
+          SAR_CHECK(kw.x + a.pair_pad >= 0 && kw.x + a.pair_pad <= a.pair_stride - a.W, 2);
           const int i0 = min(max(kw.x + a.pair_pad, 0), a.pair_stride - a.W);
           bulk_g2s(wdst + 16u * (uint32_t)(e * a.W), a.pairs + (size_t)kw.y * a.pair_stride + i0, 16u * a.W,
                    bar_full + 8 * slot);
@@ -464,7 +481,10 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     acc_i[p] = 0.f;
     fd[p] = 0.f;
     if (DOP) {
-      if (SAR_PIX_OK(gx[p], gy[p])) fd[p] = __ldg(a.dop + (size_t)(J0 + yl) * a.nx + gx[p]);
+      // clamped to the plan's declared bound: a table exceeding it gives wrong values for those
+      // pixels, never a read outside the staged window
+      if (SAR_PIX_OK(gx[p], gy[p]))
+        fd[p] = fminf(fmaxf(__ldg(a.dop + (size_t)(J0 + yl) * a.nx + gx[p]), -a.dop_max), a.dop_max);
     }
     // keep the per-pixel constants in registers: a shuffle is opaque to ptxas, which
     // otherwise re-derives them from fp64 inside the chirp loop (rematerialisation)
@@ -517,6 +537,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         for (int k = 0; k < 2; ++k) {
           const float tk = k ? hi2(TK) : lo2(TK);
           const float gf = k ? hi2(GF) : lo2(GF);
+          SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+                    __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
           const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
           float sn, cs;
@@ -562,6 +585,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const float tk = kap + kMagic;
           const float kf = tk - kMagic;
           const float gf = kap - kf;
+          SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+                    __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
           const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
           float sn, cs;
@@ -592,7 +618,10 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             const float tk = kap + kMagic;
             const float kf = tk - kMagic;
             const float gf = kap - kf;
-            const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+            SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+                    __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
+          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
             const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
             float sn, cs;
             __sincosf(C3 * gf, &sn, &cs);
@@ -639,6 +668,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
       // the last chunk of the tile to finish (threadfence-reduction pattern on a per-tile
       // counter) sums the planes in chunk order (deterministic) and stores the finished tile
       // to every peer, so the gather still overlaps other tiles
+      SAR_CHECK(chunk_e < a.ws_planes, 1);
       float2* wsp = a.ws + (size_t)chunk_e * a.ws_plane;
 #pragma unroll
       for (int p = 0; p < PB; ++p)
@@ -727,6 +757,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           // chirp chunks 1.. store their partials into workspace planes 0..; chunk 0 stores (or
           // accumulates) into the image like an unsplit launch, and the split-sum kernel then
           // adds the planes in chunk order (deterministic, unlike reductions)
+          SAR_CHECK(chunk_e - 1 < a.ws_planes, 1);
           __stcg(a.ws + (size_t)(chunk_e - 1) * a.ws_plane + (size_t)gy[p] * a.nx + gx[p], make_float2(acc_r[p], acc_i[p]));
         } else if (a.accumulate) {
           const float2 o = *dst;
@@ -789,7 +820,7 @@ struct BpKernel<true, DOP, NEAR, NCW, PB, SCATTER> {
 template <bool BI, bool DOP, bool SAFE, int NCW, int PB, bool SCATTER>
 cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   auto kern = BpKernel<BI, DOP, SAFE, NCW, PB, SCATTER>::fn;
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI, a.guard);
   // the dynamic shared-memory opt-in is per device and per kernel instantiation
   static std::atomic<int> configured_bytes[kMaxDevices];
   int cur_dev = 0;

@@ -11,3 +11,14 @@ cudaError_t launch_bp_scatter(const BpArgs& a, bool bistatic, bool doppler, bool
 }
 
 }  // namespace sar
+
+#ifdef SAR_DEBUG_CHECKS
+extern "C" int sar_debug_violations_scatter(unsigned long long* out4, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out4, sar::g_violations, sizeof(sar::g_violations));
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(sar::g_violations, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

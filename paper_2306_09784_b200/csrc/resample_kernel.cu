@@ -14,10 +14,17 @@ __global__ void polar_to_cart_kernel(const ResampleArgs a) {
     const int ix = (int)(idx % a.nx), iy = (int)(idx / a.nx);
     const double px = a.x0 + ix * a.dx - a.xc, py = a.y0 + iy * a.dy - a.yc;
     const double rr = sqrt(px * px + py * py);
-    const double th = atan2(px, py);                  // from +y toward +x
-    const double fi = (th - a.th0) / a.dth, fj = (rr - a.r0) / a.dr;
+    // bearing from +y toward +x relative to the sector centre, wrapped into [-pi, pi) (a sector
+    // may cross +-pi and th0 may be given in any period; reading A19)
+    const double half = 0.5 * (a.n_th - 1) * a.dth;
+    double db = atan2(px, py) - (a.th0 + half);
+    db -= 2.0 * kPi * floor((db + kPi) / (2.0 * kPi));
+    double fi = (db + half) / a.dth, fj = (rr - a.r0) / a.dr;
     float2 v = make_float2(0.f, 0.f);
-    if (fi >= 0.0 && fj >= 0.0 && fi <= a.n_th - 1 && fj <= a.n_r - 1) {
+    // nodes on the sector boundary count as inside (1e-9 of an index of rounding slack)
+    if (fi >= -1e-9 && fj >= -1e-9 && fi <= a.n_th - 1 + 1e-9 && fj <= a.n_r - 1 + 1e-9) {
+      fi = fmin(fmax(fi, 0.0), (double)(a.n_th - 1));
+      fj = fmin(fmax(fj, 0.0), (double)(a.n_r - 1));
       const int i0 = min((int)fi, a.n_th - 1), j0 = min((int)fj, a.n_r - 1);
       const int i1 = min(i0 + 1, a.n_th - 1), j1 = min(j0 + 1, a.n_r - 1);
       const float wi = (float)(fi - i0), wj = (float)(fj - j0);

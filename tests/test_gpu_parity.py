@@ -621,3 +621,23 @@ def test_largest_fft_and_full_crop_match_oracle(cuda_lib):
     plan.close()
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
     assert rel_err(got, ref) <= REL_TOL
+
+
+def test_bounds_check_build_counts_no_violation():
+    """The -DSAR_DEBUG_CHECKS build of the same sources (compute-sanitizer is closed on this GPU
+    pool) over every kernel family: no window index outside its item, no workspace plane out of
+    range, no clamped bulk copy for inputs within the contract, and no shared-memory read outside
+    the allocation even for an antenna outside the declared box (tools/check_cases.py)."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_2306_09784_b200 import _build
+
+    if not os.path.exists(_build.CHECK_LIB):
+        _build.build(out=_build.CHECK_LIB, defines=["-DSAR_DEBUG_CHECKS"])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "check_cases.py")], capture_output=True,
+                         text=True, timeout=600, env={**os.environ, "SAR_LIB": _build.CHECK_LIB}, cwd=root)
+    assert out.returncode == 0, out.stdout + out.stderr[-3000:]
+    assert out.stdout.count("-> ok") >= 10

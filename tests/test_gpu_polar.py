@@ -54,14 +54,18 @@ def test_polar_row_shards_equal_unsharded(cuda_lib):
     plan.close()
 
 
-def test_polar_to_cartesian_kernel_matches_oracle(cuda_lib):
+@pytest.mark.parametrize("th0", [-0.7, 2.5, -0.7 + 2 * np.pi])
+def test_polar_to_cartesian_kernel_matches_oracle(cuda_lib, th0):
+    """The resampling kernel against the oracle, also for a sector crossing +-pi (centred on -y)
+    and for th0 given in the next period."""
     import torch
 
-    pg = PolarGrid(0.1, -0.3, 0.0, 2.0, 0.03, -0.7, 0.012, 117, 61)
+    pg = PolarGrid(0.1, -0.3, 0.0, 2.0, 0.03, th0, 0.012, 117, 61)
     rng = np.random.default_rng(7)
     img = (rng.standard_normal((pg.n_r, pg.n_th)) + 1j * rng.standard_normal((pg.n_r, pg.n_th)))
     img = img.astype(np.complex64)
-    cart = Grid(-2.0, 0.5, 0.0, 0.021, 0.019, 203, 197)
+    cart = Grid(-2.0, 0.5, 0.0, 0.021, 0.019, 203, 197) if abs(np.cos(th0)) < 0.9 or np.cos(th0) > 0 \
+        else Grid(-2.0, -4.5, 0.0, 0.021, 0.019, 203, 197)
     got = cuda_lib.polar_to_cartesian(pg, torch.as_tensor(img, device="cuda:0"), cart)
     torch.cuda.synchronize()
     got = got.cpu().numpy()

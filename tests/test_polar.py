@@ -13,6 +13,11 @@ from paper_2306_09784_b200 import _build, sar
 from sarsim import C_LIGHT, Grid, PolarGrid, Radar
 
 PG = PolarGrid(0.3, -0.2, 0.0, 4.0, 0.05, -0.4, 0.01, 81, 31)
+# the same sector shape looking toward -y (bearings 2.8 .. 3.6 rad cross +-pi), and the first
+# sector with th0 given in the next period (th0 + 2 pi): bearings are angles (reading A19)
+PG_WRAP = PolarGrid(0.3, -0.2, 0.0, 4.0, 0.05, 2.8, 0.01, 81, 31)
+PG_PERIOD = PolarGrid(0.3, -0.2, 0.0, 4.0, 0.05, -0.4 + 2 * math.pi, 0.01, 81, 31)
+SECTORS = [PG, PG_WRAP, PG_PERIOD]
 
 
 def _one_pixel_grid(x, y):
@@ -24,9 +29,14 @@ def _bilinear(fi, fj):
     return (0.7 - 0.2j) + (0.03 + 0.01j) * fi + (-0.05 + 0.02j) * fj + (0.002 - 0.004j) * fi * fj
 
 
-def _polar_image(f):
-    jj, ii = np.meshgrid(np.arange(PG.n_r), np.arange(PG.n_th), indexing="ij")
+def _polar_image(f, pg=PG):
+    jj, ii = np.meshgrid(np.arange(pg.n_r), np.arange(pg.n_th), indexing="ij")
     return f(ii.astype(float), jj.astype(float))
+
+
+def _wrap(th, th0):
+    """Bearing offset from th0 in [0, 2 pi)."""
+    return np.mod(th - th0, 2 * np.pi)
 
 
 def test_polar_pixels_follow_the_definition():
@@ -41,39 +51,42 @@ def test_polar_pixels_follow_the_definition():
     assert PG.nx == PG.n_th and PG.ny == PG.n_r
 
 
-def test_resample_reproduces_bilinear_functions_exactly():
+@pytest.mark.parametrize("pg", SECTORS, ids=["ahead", "across_pi", "th0_next_period"])
+def test_resample_reproduces_bilinear_functions_exactly(pg):
     """Bilinear interpolation is exact for functions bilinear in (th, r): probe points are
-    placed by the FORWARD polar map at known fractional indices."""
-    img = _polar_image(_bilinear)
+    placed by the FORWARD polar map at known fractional indices (also for a sector crossing
+    +-pi and for th0 given in another period)."""
+    img = _polar_image(_bilinear, pg)
     rng = np.random.default_rng(3)
     for _ in range(200):
-        fi = rng.uniform(0, PG.n_th - 1)
-        fj = rng.uniform(0, PG.n_r - 1)
-        r = PG.r0 + fj * PG.dr
-        th = PG.th0 + fi * PG.dth
-        cart = _one_pixel_grid(PG.xc + r * math.sin(th), PG.yc + r * math.cos(th))
-        got = oracle.polar_to_cartesian(PG, img, cart)[0, 0]
+        fi = rng.uniform(0, pg.n_th - 1)
+        fj = rng.uniform(0, pg.n_r - 1)
+        r = pg.r0 + fj * pg.dr
+        th = pg.th0 + fi * pg.dth
+        cart = _one_pixel_grid(pg.xc + r * math.sin(th), pg.yc + r * math.cos(th))
+        got = oracle.polar_to_cartesian(pg, img, cart)[0, 0]
         assert abs(got - _bilinear(fi, fj)) < 1e-9
 
 
-def test_resample_nodes_constant_and_outside():
-    img = _polar_image(_bilinear)
-    for (j, i) in [(0, 0), (PG.n_r - 1, PG.n_th - 1), (7, 40), (30, 3)]:
-        x, y, _ = PG.pixel_list(np.array([[j, i]]))[0]
-        got = oracle.polar_to_cartesian(PG, img, _one_pixel_grid(x, y))[0, 0]
+@pytest.mark.parametrize("pg", SECTORS, ids=["ahead", "across_pi", "th0_next_period"])
+def test_resample_nodes_constant_and_outside(pg):
+    img = _polar_image(_bilinear, pg)
+    for (j, i) in [(0, 0), (pg.n_r - 1, pg.n_th - 1), (7, 40), (30, 3)]:
+        x, y, _ = pg.pixel_list(np.array([[j, i]]))[0]
+        got = oracle.polar_to_cartesian(pg, img, _one_pixel_grid(x, y))[0, 0]
         assert abs(got - img[j, i]) < 1e-9
     # a constant polar image resamples to the constant inside the sector, 0 outside
-    const = np.full((PG.n_r, PG.n_th), 2.0 - 1.0j)
-    cart = Grid(-2.5, 2.0, 0.0, 0.05, 0.05, 120, 90)
-    out = oracle.polar_to_cartesian(PG, const, cart)
+    const = np.full((pg.n_r, pg.n_th), 2.0 - 1.0j)
+    cart = Grid(pg.xc - 6.0, pg.yc - 6.0, 0.0, 0.05, 0.05, 240, 240)
+    out = oracle.polar_to_cartesian(pg, const, cart)
     pix = cart.pixels().reshape(cart.ny, cart.nx, 3)
-    d = pix[..., :2] - np.array([PG.xc, PG.yc])
+    d = pix[..., :2] - np.array([pg.xc, pg.yc])
     r = np.hypot(d[..., 0], d[..., 1])
-    th = np.arctan2(d[..., 0], d[..., 1])
-    inside = (r >= PG.r0 + 1e-9) & (r <= PG.r0 + (PG.n_r - 1) * PG.dr - 1e-9) & \
-             (th >= PG.th0 + 1e-9) & (th <= PG.th0 + (PG.n_th - 1) * PG.dth - 1e-9)
-    outside = (r < PG.r0 - 1e-9) | (r > PG.r0 + (PG.n_r - 1) * PG.dr + 1e-9) | \
-              (th < PG.th0 - 1e-9) | (th > PG.th0 + (PG.n_th - 1) * PG.dth + 1e-9)
+    b = _wrap(np.arctan2(d[..., 0], d[..., 1]), pg.th0)
+    span = (pg.n_th - 1) * pg.dth
+    inside = (r >= pg.r0 + 1e-9) & (r <= pg.r0 + (pg.n_r - 1) * pg.dr - 1e-9) & (b >= 1e-9) & (b <= span - 1e-9)
+    outside = (r < pg.r0 - 1e-9) | (r > pg.r0 + (pg.n_r - 1) * pg.dr + 1e-9) | \
+              ((b > span + 1e-9) & (b < 2 * np.pi - 1e-9))
     assert inside.sum() > 1000 and outside.sum() > 1000
     assert np.allclose(out[inside], 2.0 - 1.0j, atol=1e-12)
     assert np.all(out[outside] == 0)
