@@ -92,9 +92,9 @@ typedef struct {
 /* Declared axis-aligned bounding box of ALL antenna phase centres (TX and RX)
  * the plan will be used with.  The range crop is derived from it and the grid box
  * with the triangle inequality; positions outside it give wrong values (never an
- * out-of-bounds access: pair-row copies are clamped into their row, and a polar plan's
- * tighter window bound is backed by guard entries up to the triangle bound, which holds
- * for any position).  sar_form_image verifies its host positions against it. */
+ * out-of-bounds access: pair-row copies are clamped into their row, and a polar plan,
+ * whose tile windows are bounded with the box, clamps positions into the box).
+ * sar_form_image verifies its host positions against it. */
 typedef struct {
   double lo[3], hi[3];
 } sar_box_t;

@@ -10,8 +10,8 @@ bool bp_shape_supported(int ncw, int pb) {
   return (ncw == 8 && pb == 4) || (ncw == 4 && pb == 8) || (ncw == 4 && pb == 4) || (ncw == 8 && pb == 8);
 }
 
-size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic, int guard) {
-  return make_layout(W, CB, n_rx, S, bistatic, guard).total;
+size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic) {
+  return make_layout(W, CB, n_rx, S, bistatic).total;
 }
 
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s) {

@@ -58,6 +58,28 @@ namespace sar {
 namespace {
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+#ifndef SAR_BP_GROUP
+#define SAR_BP_GROUP 8
+#endif
+#ifndef SAR_BP_JUNROLL
+#define SAR_BP_JUNROLL 8
+#endif
+constexpr int kGroup = SAR_BP_GROUP;     // derived-chirp group (monostatic): one rsqrt per group
+constexpr int kJUnroll = SAR_BP_JUNROLL;
+#ifndef SAR_BP_DERIVE_MONO
+#define SAR_BP_DERIVE_MONO 1
+#endif
+#ifndef SAR_BP_DERIVE_BI
+#define SAR_BP_DERIVE_BI 1
+#endif
+constexpr bool kDeriveMono = SAR_BP_DERIVE_MONO;   // derived-chirp groups compiled in (monostatic)
+constexpr bool kDeriveBi = SAR_BP_DERIVE_BI;       // derived stages compiled in (bistatic)
+// Series bounds |delta| of derived legs: truncation error <= 5 R delta^4 / 128 (3 terms,
+// monostatic groups) and 7 R delta^5 / 256 (4 terms, bistatic stages), below 1.6e-10 m at R >= 1 m
+// (< 1e-6 rad of carrier phase per update: the images stay within fp32 summation order of the
+// per-chirp rsqrt form, whatever the chirp order)
+constexpr double kDeriveDelta = 0.008;
+constexpr double kDeriveDeltaBi = 0.023;
 constexpr uint32_t kMagicBits = 0x4B400000u;
 constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
 #ifndef SAR_BP_BATCH
@@ -229,29 +251,55 @@ __device__ __forceinline__ f32x2 leg_delta2(const float4 A, const f32x2 UX, cons
   return ffma2(RHO, fmul2(Q, bc2(0.5f)), T);                      // |p - q| - r
 }
 
+// Antenna phase centre as the producer uses it.  Polar plans bound each tile's window by the
+// declared antenna box (tighter than the triangle inequality): a position outside the box is
+// clamped into it, so a false declaration gives wrong values but every window read stays in
+// range.  Cartesian windows hold for any position (triangle inequality): used as given.
+struct Q3 {
+  double x, y, z;
+};
+__device__ __forceinline__ Q3 ld_pos(const double* q, const BpArgs& a) {
+  Q3 r{q[0], q[1], q[2]};
+  if (a.polar) {
+    r.x = fmin(fmax(r.x, a.box_lo[0]), a.box_hi[0]);
+    r.y = fmin(fmax(r.y, a.box_lo[1]), a.box_hi[1]);
+    r.z = fmin(fmax(r.z, a.box_lo[2]), a.box_hi[2]);
+  }
+  return r;
+}
+
+// leg_delta2 that also returns Q = rsqrt(s) ~ 1/|p - q| (derived-chirp groups)
+__device__ __forceinline__ f32x2 leg_delta2q(const float4 A, const f32x2 UX, const f32x2 UY, const f32x2 W, f32x2& Q) {
+  const f32x2 G2 = ffma2(bc2(A.x), UX, ffma2(bc2(A.y), UY, W));
+  const f32x2 S = fadd2(G2, bc2(A.z));
+  Q = pk2(rsqrt_mufu(lo2(S)), rsqrt_mufu(hi2(S)));
+  const f32x2 T = ffma2(S, Q, bc2(-A.w));
+  const f32x2 H = ffma2(S, Q, bc2(A.w));
+  const f32x2 RHO = ffma2(pk2(-lo2(T), -hi2(T)), H, G2);
+  return ffma2(RHO, fmul2(Q, bc2(0.5f)), T);
+}
+
 // Shared-memory layout (bytes, 16-B aligned):
 //   [0, 128)                     mbarriers full[kBpMaxStages], empty[kBpMaxStages]
+//   [128, 160)                   producer scratch
 //   rec   [S][LEGS] x 32 B       monostatic: LEGS = items; bistatic: LEGS = CB + items
 //   kwin  [S][items] int2        {window start bin (crop-relative), profile row}
 //   win   [S][items][W] x 16 B   pair-format profile windows
 struct Layout {
   int items, legs;
-  uint32_t rec, kwin, win, total;
+  uint32_t flags, rec, kwin, win, total;
 };
 
-//   guard: G spare entries before the first and after the last window (polar plans): a consumer
-//          index past its item's window (an antenna outside the declared box breaks the polar
-//          window bound, never the triangle bound the guard covers) reads wrong values, never
-//          outside the allocation
-__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic, int guard) {
+__host__ __device__ inline Layout make_layout(int W, int CB, int n_rx, int S, bool bistatic) {
   Layout L;
   L.items = CB * n_rx;
   L.legs = bistatic ? CB + L.items : L.items;
-  L.rec = 16 * kBpMaxStages;
+  L.flags = 16 * kBpMaxStages;   // producer scratch (derived-group flags of the stage being built)
+  L.rec = L.flags + 32;
   L.kwin = L.rec + (uint32_t)S * L.legs * 32;
   const uint32_t kw_bytes = ((uint32_t)S * L.items * 8 + 15u) & ~15u;
-  L.win = L.kwin + kw_bytes + 16u * (uint32_t)guard;
-  L.total = L.win + (uint32_t)S * L.items * W * 16 + 16u * (uint32_t)guard;
+  L.win = L.kwin + kw_bytes;
+  L.total = L.win + (uint32_t)S * L.items * W * 16;
   return L;
 }
 
@@ -263,7 +311,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   constexpr int TY = NCW * PB * kPatchX * kPatchY / kTileX;
   extern __shared__ __align__(16) unsigned char smem[];
   const int S = a.S;
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC, a.guard);
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, S, BISTATIC);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase, bar_empty = sbase + 8 * kBpMaxStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -300,6 +348,36 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
     PTy = a.y0 + (J0 + 0.5 * (TY - 1)) * a.dy;
   }
   const double PTz = a.z0;
+  // near-field test of this tile (NEAR kernels): distance from the anchor to the antenna box;
+  // rho_t = the tile's half-diagonal (polar: farthest corner from the anchor)
+  double rho_t = a.tile_rho;
+  if (a.polar) {   // annular patch: farthest from its anchor at a corner
+    const double rc = a.r0 + (J0 + 0.5 * (TY - 1)) * a.dr;
+    const double ht = 0.5 * (TX - 1) * a.dth, hr = 0.5 * (TY - 1) * a.dr;
+    rho_t = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      const double rr = rc + ((c & 1) ? hr : -hr), dt = (c & 2) ? ht : -ht;
+      rho_t = fmax(rho_t, sqrt(rr * rr + rc * rc - 2.0 * rr * rc * cos(dt)));
+    }
+  }
+  bool tile_near = false;
+  if constexpr (NEAR) {
+    double d2 = 0.0;
+    const double pt[3] = {PTx, PTy, PTz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double gap = fmax(0.0, fmax(a.box_lo[k] - pt[k], pt[k] - a.box_hi[k]));
+      d2 += gap * gap;
+    }
+    const double near_r = 3.0 * rho_t * (1.0 + 1e-6) + 1e-3;
+    tile_near = d2 < near_r * near_r;
+  }
+  // derived-chirp groups: far-field monostatic tiles of plans that allow them
+  // (derived stages only in the default 8 x 4 bistatic shape: in the 4 x 4 polar shape the extra
+  //  code alone costs registers and measured 20 % on C6p, whose short stages gain nothing)
+  constexpr bool kDerBi = kDeriveBi && NCW == 8 && PB == 4;
+  const bool derive = kDeriveMono && !BISTATIC && a.derive && !tile_near;
+  const bool derive_bi = kDerBi && BISTATIC && a.derive && !tile_near;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -336,8 +414,8 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
       // ---- anchor records (fp64), one item per lane
       if (BISTATIC) {
         for (int c = lane; c < cnt; c += 32) {
-          const double* q = a.tx + 3 * (size_t)(chirp0 + c0 + c);
-          const double Dx = PTx - q[0], Dy = PTy - q[1], Dz = PTz - q[2];
+          const Q3 q = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0 + c), a);
+          const double Dx = PTx - q.x, Dy = PTy - q.y, Dz = PTz - q.z;
           const float r = (float)sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           srec[2 * c] = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), r * r, r);
           srec[2 * c + 1] = make_float4(0.f, 0.f, NEAR ? (float)(Dz * Dz) : 0.f, 0.f);
@@ -347,7 +425,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         const int c = BISTATIC ? e / a.n_rx : e;
         const int n = BISTATIC ? e - c * a.n_rx : 0;
         const int m = chirp0 + c0 + c;
-        const double* qt = a.tx + 3 * (size_t)m;
+        const Q3 qt = ld_pos(a.tx + 3 * (size_t)m, a);
         // The consumers form r32 + dR = sqrt(r32^2 + 2 D32.u + |u|^2) from the fp32-rounded
         // record; the anchor path length uses the exact fp64 |D| so that the rounding of
         // r and D enters only at second order (|r32 - |D|| * dR / r, ~1e-8 m).
@@ -355,16 +433,16 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         float4 leg0;
         float rleg;
         if (BISTATIC) {
-          const double* qr = a.rx + 3 * ((size_t)m * a.n_rx + n);
-          const double Dx = PTx - qr[0], Dy = PTy - qr[1], Dz = PTz - qr[2];
+          const Q3 qr = ld_pos(a.rx + 3 * ((size_t)m * a.n_rx + n), a);
+          const double Dx = PTx - qr.x, Dy = PTy - qr.y, Dz = PTz - qr.z;
           const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           rleg = (float)rr;
           leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
           dz = Dz;
-          const double Tx = PTx - qt[0], Ty = PTy - qt[1], Tz = PTz - qt[2];
+          const double Tx = PTx - qt.x, Ty = PTy - qt.y, Tz = PTz - qt.z;
           d_anchor = sqrt(Tx * Tx + Ty * Ty + Tz * Tz) + rr;
         } else {
-          const double Dx = PTx - qt[0], Dy = PTy - qt[1], Dz = PTz - qt[2];
+          const double Dx = PTx - qt.x, Dy = PTy - qt.y, Dz = PTz - qt.z;
           const double rr = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
           rleg = (float)rr;
           leg0 = make_float4((float)(2.0 * Dx), (float)(2.0 * Dy), rleg * rleg, rleg);
@@ -381,6 +459,97 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         srec[2 * ri + 1] = make_float4((float)(kap - k0 - 0.5 - wh), __uint_as_float(off),
                                        NEAR ? (float)(dz * dz) : 0.f, 0.f);
         skw[e] = make_int2(k0, m * a.n_rx + n);   // profile row (size_t offsets below: rows x n_bins may exceed 2^31)
+      }
+      if (BISTATIC && derive_bi && cnt >= 4) {   // (short stages: the base leg does not amortise)
+        // Derived stage (bistatic): every leg of the stage -- the TX legs of chirps 1.. and all
+        // RX legs -- follows from chirp 0's TX leg (the stage base b) by the series of the
+        // monostatic groups, with o = q_leg - q_tx(b) (RX offsets included), so the consumers
+        // spend one rsqrt per pixel per stage.  Records: TX of chirp c >= 1 and every RX item
+        // {-2 o_x, -2 o_y, -2 D_b.o + |o|^2, -}; RX anchor indices at 2 r_b (windows their own).
+        // Bound per leg (4-term series): (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 <= kDeriveDeltaBi.
+        volatile int* gflag = reinterpret_cast<volatile int*>(smem + L.flags);
+        __syncwarp();   // the stage's records (other lanes) are complete
+        if (lane == 0) gflag[0] = 1;
+        __syncwarp();
+        const Q3 qb = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0), a);
+        const double Dbx = PTx - qb.x, Dby = PTy - qb.y, Dbz = PTz - qb.z;
+        const double rb = sqrt(Dbx * Dbx + Dby * Dby + Dbz * Dbz), rmin = rb - rho_t;
+        auto leg_o = [&](int k, double& ox, double& oy, double& oz) {   // k < items: RX item, else TX chirp
+          const Q3 q = ld_pos(k < items ? a.rx + 3 * ((size_t)(chirp0 + c0) * a.n_rx + k)
+                                        : a.tx + 3 * (size_t)(chirp0 + c0 + (k - items)), a);
+          ox = q.x - qb.x;
+          oy = q.y - qb.y;
+          oz = q.z - qb.z;
+        };
+        for (int k = lane; k < items + cnt; k += 32) {
+          double ox, oy, oz;
+          leg_o(k, ox, oy, oz);
+          const double on = sqrt(ox * ox + oy * oy + oz * oz);
+          if (!(rmin > 0.0 && (2.0 * (rb + rho_t) * on + on * on) <= kDeriveDeltaBi * rmin * rmin)) gflag[0] = 0;
+        }
+        __syncwarp();
+        if (gflag[0]) {
+          for (int k = lane; k < items + cnt; k += 32) {
+            if (k == items) continue;   // chirp 0's TX leg stays the base leg
+            double ox, oy, oz;
+            leg_o(k, ox, oy, oz);
+            const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
+            const float4 rec_o = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
+            if (k < items) {
+              srec[2 * (a.CB + k)] = rec_o;
+              const int k0 = skw[k].x, wh = a.W >> 1;
+              srec[2 * (a.CB + k) + 1].x = (float)(a.a1 * 2.0 * rb - a.k_lo - k0 - 0.5 - wh);
+            } else {
+              srec[2 * (k - items)] = rec_o;
+            }
+          }
+          if (lane == 0) srec[1].w = 1.f;   // chirp 0's TX record: the stage is derived
+        }
+        __syncwarp();
+      }
+      if (!BISTATIC && derive) {
+        // Derived-chirp groups (monostatic): within a group of kGroup consecutive chirps of the
+        // stage, chirp j's range follows from the group base b's by the convergent series
+        //   |p - q_j| = R_b sqrt(1 + delta),  delta = E / R_b^2,
+        //   E = |p - q_j|^2 - |p - q_b|^2 = -2 (D_b + u).o + |o|^2,  o = q_j - q_b, D_b = P_T - q_b,
+        // so the consumers spend one rsqrt per pixel per group instead of per chirp.  The record
+        // of a derived chirp is {-2 o_x, -2 o_y, c = -2 D_b.o + |o|^2 (fp64 -> fp32), -} and its
+        // anchor index is taken at the base's anchor distance (its window start is its own).  A
+        // group is derived only when the series bound holds over the whole tile:
+        //   |delta| <= (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 <= kDeriveDelta
+        // (any track, any chirp order: otherwise every chirp of the group keeps its own leg).
+        __syncwarp();
+        for (int e0 = 0; e0 < items; e0 += 32) {
+          const int c = e0 + lane;
+          const int cb = c - (c % kGroup);
+          bool ok = c < cnt && cb + kGroup <= cnt;
+          double ox = 0, oy = 0, oz = 0, Dbx = 0, Dby = 0, Dbz = 0, rb = 0;
+          if (ok) {
+            const Q3 qj = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0 + c), a);
+            const Q3 qb = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0 + cb), a);
+            ox = qj.x - qb.x;
+            oy = qj.y - qb.y;
+            oz = qj.z - qb.z;
+            Dbx = PTx - qb.x;
+            Dby = PTy - qb.y;
+            Dbz = PTz - qb.z;
+            rb = sqrt(Dbx * Dbx + Dby * Dby + Dbz * Dbz);
+            const double on = sqrt(ox * ox + oy * oy + oz * oz), rmin = rb - rho_t;
+            ok = rmin > 0.0 && (2.0 * (rb + rho_t) * on + on * on) <= kDeriveDelta * rmin * rmin;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          const bool grp = ((bal >> (lane & ~(kGroup - 1))) & ((1u << kGroup) - 1)) == ((1u << kGroup) - 1);
+          if (c < cnt && grp) {
+            if (c == cb) {
+              srec[2 * c + 1].w = 1.f;   // base record: the group is derived
+            } else {
+              const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
+              srec[2 * c] = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
+              const int k0 = skw[c].x, wh = a.W >> 1;
+              srec[2 * c + 1].x = (float)(a.a1 * 2.0 * rb - a.k_lo - k0 - 0.5 - wh);
+            }
+          }
+        }
       }
       __syncwarp();
       if (a.pairs) {
@@ -538,7 +707,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const float tk = k ? hi2(TK) : lo2(TK);
           const float gf = k ? hi2(GF) : lo2(GF);
           SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
-          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
           const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
@@ -549,11 +718,73 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         }
       };
       if (!BISTATIC) {
-#pragma unroll kChirpUnroll
-        for (int c = 0; c < cnt; ++c) {
+        for (int c = 0; c < cnt;) {
           const float4 A = srec[2 * c], B = srec[2 * c + 1];
+          if (kDeriveMono && B.w != 0.f) {
+            // derived group (warp-uniform: one record for all): the base chirp's leg, then the
+            // kGroup - 1 others by the series  |p - q_j| - r_b = dR_b + (E Q) P(delta),
+            // delta = E Q^2 (Q = 1/R_b), P = 1/2 - delta/8 + delta^2/16  (truncation 5 delta^4 / 128)
+            f32x2 DR0[PB / 2], Q0[PB / 2];
 #pragma unroll
-          for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.x, __float_as_uint(B.y));
+            for (int h = 0; h < PB / 2; ++h) {
+              DR0[h] = leg_delta2q(A, UX[h], UY[h], W2[h], Q0[h]);
+              tail(h, DR0[h], B.x, __float_as_uint(B.y));
+            }
+#pragma unroll kJUnroll
+            for (int j = 1; j < kGroup; ++j) {
+              const float4 Aj = srec[2 * (c + j)], Bj = srec[2 * (c + j) + 1];
+#pragma unroll
+              for (int h = 0; h < PB / 2; ++h) {
+                const f32x2 E = ffma2(bc2(Aj.x), UX[h], ffma2(bc2(Aj.y), UY[h], bc2(Aj.z)));
+                const f32x2 EQ = fmul2(E, Q0[h]);      // ~ R_b delta
+                const f32x2 D = fmul2(EQ, Q0[h]);      // delta
+                const f32x2 P = ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f));
+                tail(h, ffma2(EQ, P, DR0[h]), Bj.x, __float_as_uint(Bj.y));
+              }
+            }
+            c += kGroup;
+          } else {
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) tail(h, leg_delta2(A, UX[h], UY[h], W2[h]), B.x, __float_as_uint(B.y));
+            ++c;
+          }
+        }
+      } else if (kDerBi && srec[1].w != 0.f) {
+        // derived stage (bistatic): chirp 0's TX leg by rsqrt; every other leg l of the stage by
+        // |p - q_l| - r_b = dR_b + (E Q) P4(delta), delta = E Q^2,
+        // P4 = 1/2 - delta/8 + delta^2/16 - 5 delta^3/128; d_hyp - 2 r_b = 2 dR_b + X_tx + X_rx
+        const float4 T0 = srec[0];
+        f32x2 DR2[PB / 2], Q0[PB / 2];
+#pragma unroll
+        for (int h = 0; h < PB / 2; ++h) {
+          const f32x2 d0 = leg_delta2q(T0, UX[h], UY[h], W2[h], Q0[h]);
+          DR2[h] = fadd2(d0, d0);
+        }
+        auto xleg = [&](const float4 R, const int h, const f32x2 base) {   // base + (E Q) P4(delta), leg of record R
+          const f32x2 E = ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
+          const f32x2 EQ = fmul2(E, Q0[h]);
+          const f32x2 D = fmul2(EQ, Q0[h]);
+          const f32x2 P = ffma2(D, ffma2(D, ffma2(D, bc2(-0.0390625f), bc2(0.0625f)), bc2(-0.125f)), bc2(0.5f));
+          return ffma2(EQ, P, base);
+        };
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+          f32x2 TS[PB / 2];
+          if (c == 0) {
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) TS[h] = DR2[h];
+          } else {
+            const float4 T = srec[2 * c];
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) TS[h] = xleg(T, h, DR2[h]);
+          }
+          const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
+#pragma unroll kRxUnroll
+          for (int n = 0; n < a.n_rx; ++n, rp += 2) {
+            const float4 A = rp[0], B = rp[1];
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+          }
         }
       } else {
 #pragma unroll 1
@@ -563,8 +794,13 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 #pragma unroll
           for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
           const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
+#ifdef SAR_BP_EXP_NRX
+#pragma unroll
+          for (int n = 0; n < SAR_BP_EXP_NRX; ++n, rp += 2) {
+#else
 #pragma unroll kRxUnroll
           for (int n = 0; n < a.n_rx; ++n, rp += 2) {
+#endif
             const float4 A = rp[0], B = rp[1];
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h)
@@ -586,7 +822,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const float kf = tk - kMagic;
           const float gf = kap - kf;
           SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
-          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
           const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
@@ -619,7 +855,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             const float kf = tk - kMagic;
             const float gf = kap - kf;
             SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
-          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win - 16u * a.guard &&
+          SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
           const float4 e = lds128(__float_as_uint(tk) * 16u + off);
             const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
@@ -770,26 +1006,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   }
   };
   if constexpr (NEAR) {
-    // near-field test of this tile: distance from the anchor to the antenna box
-    double d2 = 0.0;
-    const double pt[3] = {PTx, PTy, PTz};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double gap = fmax(0.0, fmax(a.box_lo[k] - pt[k], pt[k] - a.box_hi[k]));
-      d2 += gap * gap;
-    }
-    double rho_t = a.tile_rho;
-    if (a.polar) {   // annular patch: farthest from its anchor at a corner
-      const double rc = a.r0 + (J0 + 0.5 * (TY - 1)) * a.dr;
-      const double ht = 0.5 * (TX - 1) * a.dth, hr = 0.5 * (TY - 1) * a.dr;
-      rho_t = 0.0;
-      for (int c = 0; c < 4; ++c) {
-        const double rr = rc + ((c & 1) ? hr : -hr), dt = (c & 2) ? ht : -ht;
-        rho_t = fmax(rho_t, sqrt(rr * rr + rc * rc - 2.0 * rr * rc * cos(dt)));
-      }
-    }
-    const double near_r = 3.0 * rho_t * (1.0 + 1e-6) + 1e-3;
-    if (d2 < near_r * near_r) consume(std::true_type{});
+    if (tile_near) consume(std::true_type{});
     else consume(std::false_type{});
   } else {
     consume(std::false_type{});
@@ -800,12 +1017,23 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 // schedule and was measured 5 % slower on C3); the bistatic kernel (TX leg kept live across
 // the RX loop) is held to four resident CTAs per SM at the default 32 x 32 tile:
 // C4 1343 -> 1190 ms (tools/vsweep.sh).
+#ifndef SAR_BP_MONO_MINB
+#define SAR_BP_MONO_MINB 4
+#endif
+// resident-CTA floor per shape (register cap ~56-113): ptxas otherwise spends registers on ILP of
+// the unrolled derived groups (4 x 4: 64 -> 120 registers) and the occupancy collapses
+constexpr int mono_min_blocks(int ncw, int pb) {
+  return ncw == 8 && pb == 4 ? SAR_BP_MONO_MINB : ncw == 4 && pb == 4 ? 6 : ncw == 4 && pb == 8 ? 4 : 2;
+}
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
-__global__ void __launch_bounds__((NCW + 1) * 32) bp_kernel_mono(const BpArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, mono_min_blocks(NCW, PB)) bp_kernel_mono(const BpArgs a) {
   bp_body<false, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? 4 : 1) bp_kernel_bi(const BpArgs a) {
+#ifndef SAR_BP_EXP_BI_MINB
+#define SAR_BP_EXP_BI_MINB 4
+#endif
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? SAR_BP_EXP_BI_MINB : 1) bp_kernel_bi(const BpArgs a) {
   bp_body<true, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool BI, bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
@@ -820,7 +1048,7 @@ struct BpKernel<true, DOP, NEAR, NCW, PB, SCATTER> {
 template <bool BI, bool DOP, bool SAFE, int NCW, int PB, bool SCATTER>
 cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   auto kern = BpKernel<BI, DOP, SAFE, NCW, PB, SCATTER>::fn;
-  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI, a.guard);
+  const Layout L = make_layout(a.W, a.CB, a.n_rx, a.S, BI);
   // the dynamic shared-memory opt-in is per device and per kernel instantiation
   static std::atomic<int> configured_bytes[kMaxDevices];
   int cur_dev = 0;

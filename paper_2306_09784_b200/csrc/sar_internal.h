@@ -51,8 +51,8 @@ struct BpArgs {
   int ty0, ntile, tile_lo, tile_hi;
   int ksplit, chunk;        // chirp split (launcher): ksplit chunks of `chunk` chirps
   int W;                   // window bins per item
-  int guard;               // spare window entries at both ends of the ring (polar plans)
   float dop_max;           // declared |f_doppler| bound (bins): the table is clamped to it
+  int derive;              // 1: derived-chirp groups allowed (monostatic far-field tiles)
   int CB;                  // chirps per ring stage
   int S;                   // ring stages (<= kBpMaxStages)
   int ncw, pb;             // CTA shape: consumer warps, pixels per consumer thread
@@ -87,7 +87,7 @@ struct BpArgs {
 };
 
 bool bp_shape_supported(int ncw, int pb);
-size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic, int guard);
+size_t bp_smem_bytes(int W, int CB, int n_rx, int S, bool bistatic);
 cudaError_t launch_rc(const RcArgs& a, cudaStream_t s);
 int rc_path(int ns, int nfft, bool allow_env = true);   // 0: classic shared-memory FFT, else the register path's L
 cudaError_t launch_bp(const BpArgs& a, bool bistatic, bool doppler, bool near, cudaStream_t s);
@@ -150,7 +150,6 @@ struct sar_plan_s {
   int device;
   bool near_field;         // an antenna may come within 2 rho of a tile anchor
   int bp_ncw, bp_pb, bp_stages;
-  int bp_guard;            // smem guard entries (polar: triangle bound minus the polar window bound)
   double tile_rho;         // tile half-diagonal (m), max over tiles
   double win_rho;          // per-leg half spread of |p - q| over a tile (m): sets kap_half
   float rc_scale;

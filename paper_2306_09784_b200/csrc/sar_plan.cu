@@ -48,7 +48,6 @@ struct Derived {
   double win_rho;   // per-leg half spread of |p - q| over a tile, max over tiles (window)
   bool near_field;
   int ncw, pb, stages;
-  int guard = 0;           // BP smem guard entries (polar plans)
 };
 
 // Polar grid (Measure E) -> bounding box of the annular sector and a Cartesian stand-in
@@ -237,9 +236,6 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
     break;
   }
   const double kap_half = 2.0 * I.a1_bins_per_m * out->win_rho + dop;
-  // a consumer index stays within 2 a1 (rho - win_rho) entries of its window whatever the antenna
-  // position (triangle inequality); polar windows are tighter than that: guard entries
-  out->guard = pg ? (int)ceil(2.0 * I.a1_bins_per_m * std::max(0.0, out->rho - out->win_rho)) + 2 : 0;
   const double w = ceil(2.0 * kap_half) + 4.0;
   if (w > 4096.0)
     return fail(SAR_ERR_INVALID_ARGUMENT,
@@ -250,7 +246,7 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   const bool bistatic = r->n_rx > 1;
   const bool auto_cb = cb <= 0, auto_stages = stages <= 0;
   auto smem = [&](int cb_, int st) {
-    return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic, out->guard);
+    return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic);
   };
   if (auto_cb) {
     cb = std::max(1, 32 / r->n_rx);
@@ -412,7 +408,6 @@ static sar_status_t create_impl(const sar_radar_params_t* radar, const sar_grid_
   p->bp_ncw = d.ncw;
   p->bp_pb = d.pb;
   p->bp_stages = d.stages;
-  p->bp_guard = d.guard;
   {
     // per-device pool for the per-call pair-format rows: stream-ordered allocations that stay
     // warm across calls and plans (C5's frame plans share it); created once, never released
@@ -691,7 +686,10 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
   a.pb = plan->bp_pb;
   a.accumulate = accumulate;
   a.W = plan->info.window_bins;
-  a.guard = plan->bp_guard;
+  {   // tuning / test switch, read per call: SAR_BP_DERIVE=0 keeps one rsqrt leg per chirp
+    const char* e = getenv("SAR_BP_DERIVE");
+    a.derive = e && e[0] == '0' ? 0 : 1;
+  }
   a.dop_max = r.doppler_max_bins;
   a.CB = plan->info.chirps_per_stage;
   a.x0 = g.x0;

@@ -1,6 +1,8 @@
 """GPU parity (-m gpu): the CUDA path through the C ABI against the fp64 oracle on the same
 seeded inputs.  Bar (north star): peak pixel indices equal and
 max|img_gpu - img_ref| / max|img_ref| <= 1e-3; profiles within 1e-5 of max|ref|."""
+import os
+
 import numpy as np
 import pytest
 
@@ -149,15 +151,29 @@ def test_translation_invariance_gpu(cuda_lib):
     assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
 
 
-def test_chirp_permutation_gpu(cuda_lib):
-    scn = sarsim.small_config(n_chirps=96, ns=256, nx=40, ny=30, curved=True, n_rx=2, seed=32)
+@pytest.mark.parametrize("n_rx", [1, 2])
+def test_chirp_permutation_gpu(cuda_lib, n_rx, monkeypatch):
+    """T6 on the GPU.  With one rsqrt leg per chirp (SAR_BP_DERIVE=0) the image is order-invariant
+    to fp32 summation order (1e-5).  By default, groups of consecutive chirps whose positions are
+    close take their legs from the group base by the series (reading A22); a permutation breaks
+    the groups up, so the two images differ by the series' rounding (<= 1e-8 m per leg, checked
+    at 1e-4) and both meet the oracle bar."""
+    scn = sarsim.small_config(n_chirps=96, ns=256, nx=40, ny=30, curved=True, n_rx=n_rx, seed=32)
     raw = _raw(scn)
-    a = gpu_image(scn, raw).cpu().numpy()
     perm = np.random.default_rng(2).permutation(96)
-    scn2 = Scenario("perm", scn.radar, scn.grid, scn.tx[perm], scn.rx[perm], scn.targets, scn.amps,
-                    scn.isolated, scn.wsar[perm])
-    b = gpu_image(scn2, raw[perm.tolist()].contiguous()).cpu().numpy()
-    assert rel_err(b, a) < 1e-5
+    rx = None if scn.rx is None else scn.rx[perm]
+    scn2 = Scenario("perm", scn.radar, scn.grid, scn.tx[perm], rx, scn.targets, scn.amps, scn.isolated,
+                    scn.wsar[perm])
+    raw2 = raw[perm.tolist()].contiguous()
+    a = gpu_image(scn, raw).cpu().numpy()
+    b = gpu_image(scn2, raw2).cpu().numpy()
+    ref = oracle_image(scn, raw.cpu().numpy()).reshape(a.shape)
+    assert rel_err(b, a) < 1e-4
+    assert rel_err(a, ref) <= REL_TOL and rel_err(b, ref) <= REL_TOL
+    monkeypatch.setenv("SAR_BP_DERIVE", "0")
+    a0 = gpu_image(scn, raw).cpu().numpy()
+    b0 = gpu_image(scn2, raw2).cpu().numpy()
+    assert rel_err(b0, a0) < 1e-5
 
 
 def test_doppler_term_matches_oracle(cuda_lib):
@@ -252,6 +268,15 @@ def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
     plan.backproject_tiles(prof, tx, 4, 1, rx, out=one)   # tile (1, 1): only its pixels written
     acc = plan.backproject(prof, tx, rx, chirp0=0, nchirp=37)
     plan.backproject(prof, tx, rx, chirp0=37, nchirp=63, out=acc, accumulate=True)
+    # chirp shards regroup the derived legs (reading A22): fp32 order + the series' rounding;
+    # with one rsqrt leg per chirp, fp32 summation order only
+    os.environ["SAR_BP_DERIVE"] = "0"
+    try:
+        full0 = plan.backproject(prof, tx, rx)
+        acc0 = plan.backproject(prof, tx, rx, chirp0=0, nchirp=37)
+        plan.backproject(prof, tx, rx, chirp0=37, nchirp=63, out=acc0, accumulate=True)
+    finally:
+        del os.environ["SAR_BP_DERIVE"]
     torch.cuda.synchronize()
     a = img.cpu().numpy()
     assert torch.equal(aligned, img)
@@ -260,7 +285,8 @@ def test_row_and_chirp_shards_equal_unsharded(cuda_lib):
     mask = torch.zeros((90, 70), dtype=torch.bool, device="cuda:0")
     mask[ty:2 * ty, 32:64] = True
     assert torch.equal(one[mask], img[mask]) and torch.all(one[~mask] == sentinel)
-    assert rel_err(acc.cpu().numpy(), a) < 1e-5
+    assert rel_err(acc.cpu().numpy(), a) < 1e-4
+    assert rel_err(acc0.cpu().numpy(), full0.cpu().numpy()) < 1e-5
     # empty chirp shard: zeros (overwrite) / untouched (accumulate); empty row/tile shard: no-op
     z = plan.backproject(prof, tx, rx, chirp0=10, nchirp=0)
     keep = acc.clone()

@@ -64,8 +64,9 @@ def test_polar_to_cartesian_kernel_matches_oracle(cuda_lib, th0):
     rng = np.random.default_rng(7)
     img = (rng.standard_normal((pg.n_r, pg.n_th)) + 1j * rng.standard_normal((pg.n_r, pg.n_th)))
     img = img.astype(np.complex64)
-    cart = Grid(-2.0, 0.5, 0.0, 0.021, 0.019, 203, 197) if abs(np.cos(th0)) < 0.9 or np.cos(th0) > 0 \
-        else Grid(-2.0, -4.5, 0.0, 0.021, 0.019, 203, 197)
+    # a grid around the sector: ahead of the centre (+y) or behind it (-y)
+    ahead = np.cos(th0 + 0.5 * (pg.n_th - 1) * pg.dth) > 0
+    cart = Grid(-2.0, 0.5, 0.0, 0.021, 0.019, 203, 197) if ahead else Grid(-2.0, -4.5, 0.0, 0.021, 0.019, 203, 197)
     got = cuda_lib.polar_to_cartesian(pg, torch.as_tensor(img, device="cuda:0"), cart)
     torch.cuda.synchronize()
     got = got.cpu().numpy()

@@ -2,7 +2,7 @@
 tools/variants/libsar_check.so via SAR_LIB): range compression (register and classic paths), plain
 BP (unsplit and chirp-split with the split-sum kernel), near-field tiles (side stream), bistatic,
 Doppler (incl. a table exceeding its declared bound: clamped), polar + resampling (incl. an antenna
-outside the declared box: guard entries), the split-publish scatter, tile shards, sar_image_sum.
+outside the declared box: clamped into it), the split-publish scatter, tile shards, sar_image_sum.
 (tools/variants/libsar_check.so was the tuning-build name; __graft_entry__.build() makes
 paper_2306_09784_b200/libsar_check.so.)
 compute-sanitizer is closed on this GPU pool, so the kernels count their own violations (window
@@ -157,8 +157,8 @@ def case_doppler_over_bound():
 
 
 def case_polar_antenna_outside_box():
-    """Positions outside the declared box break the polar window bound (not the triangle bound):
-    the guard entries keep every read inside the allocation (values are wrong, by contract)."""
+    """Positions outside the declared box would break the polar window bound: a polar plan clamps
+    them into the box, so every window read stays in range (values are wrong, by contract)."""
     scn = sarsim.polar_small_config(n_chirps=64, ns=256, n_th=70, n_r=40, seed=10)
     raw = sarsim.simulate_raw(scn, device="cuda:0")
     lo, hi = scn.antenna_box(1e-3)

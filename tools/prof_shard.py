@@ -5,6 +5,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("SAR_PKG_ROOT"):   # tuning: another build's package (e.g. a previous commit)
+    sys.path.insert(0, os.environ["SAR_PKG_ROOT"])
 import torch
 
 import sarsim
