@@ -156,6 +156,10 @@ __device__ __forceinline__ unsigned ctaid_x() {   // opaque to CSE: not kept liv
   return v;
 }
 
+// window entry address of rounded index bits tk (1.5 * 2^23 + K): 16 B per entry from `off`
+// (one IMAD; written as shift + add, ptxas emits the same IMAD)
+__device__ __forceinline__ uint32_t win_addr(float tk, uint32_t off) { return __float_as_uint(tk) * 16u + off; }
+
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -709,7 +713,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
           SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
-          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const float4 e = lds128(win_addr(tk, off));
           const f32x2 V = ffma2(bc2(gf), pk2(e.z, e.w), pk2(e.x, e.y));             // lerp (re, im)
           float sn, cs;
           __sincosf(k ? hi2(TH) : lo2(TH), &sn, &cs);
@@ -824,7 +828,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
           SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
-          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const float4 e = lds128(win_addr(tk, off));
           const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
           float sn, cs;
           __sincosf(C3 * gf, &sn, &cs);
@@ -857,7 +861,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             SAR_CHECK((unsigned)((int)(__float_as_uint(tk) - kMagicBits) + (a.W >> 1)) < (unsigned)a.W, 0);
           SAR_CHECK(__float_as_uint(tk) * 16u + off >= sbase + L.win &&
                     __float_as_uint(tk) * 16u + off + 16u <= sbase + L.total, 3);
-          const float4 e = lds128(__float_as_uint(tk) * 16u + off);
+          const float4 e = lds128(win_addr(tk, off));
             const float vr = fmaf(gf, e.z, e.x), vi = fmaf(gf, e.w, e.y);
             float sn, cs;
             __sincosf(C3 * gf, &sn, &cs);

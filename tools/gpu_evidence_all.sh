@@ -10,7 +10,7 @@ for c in C0 C2 C4 C5 C5i C6 C6p; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/configs/bench_$c.json 2> gpurun_out/configs/bench_$c.err; echo $c rc=$?
 done
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_small.log 2>&1 && \
-  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rc_kernel|bp_kernel|pair_kernel" --csv \
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rc_kernel|bp_kernel|pair_kernel|split_sum" --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo launches_rc=$?
 timeout 300 python tools/prof_bp.py C3 2 > gpurun_out/plain_prof.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bp_kernel|rc_kernel|pair_kernel" -s 3 -c 3 \
