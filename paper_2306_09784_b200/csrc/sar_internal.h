@@ -169,8 +169,5 @@ struct sar_plan_s {
   float2* w_prof = nullptr;
   float2* w_img = nullptr;
   cudaMemPool_t pool = nullptr;   // device pool of the per-call pair-format rows (not owned)
-  // side stream of the near-field tile runs (concurrent with the far-field launch), lazily created
-  std::mutex side_mutex;
-  cudaStream_t side = nullptr;
   std::atomic<int64_t> launches{0};
 };

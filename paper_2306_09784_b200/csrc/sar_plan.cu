@@ -314,7 +314,6 @@ void free_plan(sar_plan_s* p) {
   cudaFree(p->w_dop);
   cudaFree(p->w_prof);
   cudaFree(p->w_img);
-  if (p->side) cudaStreamDestroy(p->side);
   delete p;
 }
 
@@ -792,33 +791,15 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     return e && e[0] == '1';
   }();
   // One launch per run of tiles: a plan with near-field tiles runs them (and only them) on the
-  // kernel with the per-tile SAFE branch; every other tile runs on the fast kernel.
+  // kernel with the per-tile SAFE branch; every other tile runs on the fast kernel (C0: near-field
+  // rows 18.3 -> 13.0 ms in round 1 by the per-tile branch; separate launches 10.48 -> 9.95 ms).
   std::vector<TileRun> runs = tile_runs(plan, tile0, ntile, tiles_x);
   cudaError_t e = cudaSuccess;
   int64_t launched = pairs ? 1 : 0;
-  // near-field runs next to far-field ones go to the plan's side stream (fork / join events), so
-  // the small near-field launch shares the GPU with the far-field one instead of following it
-  bool have_near = false, have_far = false;
-  for (const TileRun& run : runs) (run.near ? have_near : have_far) = true;
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  if (have_near && have_far) {
-    std::lock_guard<std::mutex> lock(plan->side_mutex);
-    if (!plan->side && cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking) != cudaSuccess) {
-      cudaGetLastError();
-      plan->side = nullptr;
-    }
-    side = plan->side;
-  }
-  if (side && (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-               cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess ||
-               cudaEventRecord(fork, (cudaStream_t)stream) != cudaSuccess ||
-               cudaStreamWaitEvent(side, fork, 0) != cudaSuccess)) {
-    cudaGetLastError();
-    side = nullptr;   // serial fallback on the caller's stream
-  }
+  // (the runs share the caller's stream: a side stream for the near-field runs measured no faster
+  //  on C0 with the L2 flushed between steps, and its step time varied by +-3 %)
   for (const TileRun& run : runs) {
-    void* const rstream = (side && run.near) ? (void*)side : (void*)stream;
+    void* const rstream = stream;
     sar::BpArgs b = a;
     b.ty0 = run.tile0 / tiles_x;   // the launch covers whole tile rows; [tile_lo, tile_hi) compute
     b.tile_lo = run.tile0 - b.ty0 * tiles_x;
@@ -883,12 +864,6 @@ sar_status_t backproject_impl(sar_plan_t plan, const sar_complex64_t* profiles, 
     if (b.tile_count) cudaFreeAsync(b.tile_count, (cudaStream_t)rstream);
     if (e != cudaSuccess) break;
   }
-  if (side) {
-    if (cudaEventRecord(join, side) == cudaSuccess) cudaStreamWaitEvent((cudaStream_t)stream, join, 0);
-    else cudaStreamSynchronize(side);
-  }
-  if (fork) cudaEventDestroy(fork);
-  if (join) cudaEventDestroy(join);
   if (pairs) cudaFreeAsync(pairs, (cudaStream_t)stream);
   plan->launches.fetch_add(launched);
   if (e != cudaSuccess) return cuda_fail(e, "back-projection launch");
