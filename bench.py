@@ -264,6 +264,9 @@ def run_ours(args):
     dev = torch.device(f"cuda:{local}")
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif args.all_legs:   # check run on one GPU: a one-rank group, both gather legs and their checks
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=dev)
+    dist_on = world > 1 or args.all_legs
     sar.load()
 
     scn, raw = _setup(args.config, dev)
@@ -283,9 +286,9 @@ def run_ours(args):
     per = max(n for _, n in parts)
     local_buf = plan.empty_image(per)   # a block of `per` rows: the NCCL leg gathers equal chunks
     local_img = local_buf[:nrow]
-    full_img = torch.empty((per * world, g.nx), dtype=torch.complex64, device=dev) if world > 1 else local_img
+    full_img = torch.empty((per * world, g.nx), dtype=torch.complex64, device=dev) if dist_on else local_img
     fused, fused_err = None, None
-    if world > 1 and args.gather in ("auto", "fused", "multicast"):
+    if dist_on and args.gather in ("auto", "fused", "multicast"):
         from paper_2306_09784_b200.dist import FusedRowGather
 
         try:
@@ -316,14 +319,14 @@ def run_ours(args):
         ev[1].record(stream)
         plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=local_img, stream=stream)
         ev[2].record(stream)
-        if world > 1:
+        if dist_on:
             # equal chunks of `per` rows (a short last tile-row block carries padding rows)
             dist.all_gather_into_tensor(torch.view_as_real(full_img).view(-1), torch.view_as_real(local_buf).view(-1))
         if polar:
             sar.polar_to_cartesian(g, image_of_nccl(), cart, out=cart_img, stream=stream)
 
     def image_of_nccl():
-        if world == 1:
+        if not dist_on:
             return full_img
         if all(n == per for _, n in parts):
             return full_img[: g.ny]
@@ -335,7 +338,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         step_ms, bp_ms, rc_ms, coll_ms = [], [], [], []
         l0 = plan.launches
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
@@ -350,11 +353,11 @@ def run_ours(args):
                 bp_ms.append(ev[1].elapsed_time(ev[2]))
                 coll_ms.append(ev[2].elapsed_time(ev[3]))
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         mine = torch.tensor([sum(step_ms), sum(bp_ms), sum(rc_ms), sum(coll_ms)], dtype=torch.float64, device=dev)
         allr = [torch.zeros_like(mine) for _ in range(world)]
-        if world > 1:
+        if dist_on:
             dist.all_gather(allr, mine)
         else:
             allr = [mine]
@@ -369,7 +372,8 @@ def run_ours(args):
     legs["nccl"] = timed(step_nccl)
     # ---------------- outside the timed regions: every leg's image against this plan's 1-GPU image
     # (every pixel is computed in its absolute tile: equal up to the fp32 order of chirp-chunk sums)
-    if world > 1:
+    # (the DESIGN's "<= 1e-6" is the measured rank-partition case; the check allows T11's 1e-5)
+    if dist_on:
         ref = plan.backproject(prof, tx, rx, stream=stream)
         torch.cuda.synchronize()
         scale = ref.abs().max().clamp_min(1e-30)
@@ -378,7 +382,9 @@ def run_ours(args):
             imgs["fused"] = fused.image
         for name, im in imgs.items():
             rel = float((im - ref).abs().max() / scale)
-            check[name] = {"max_rel_diff_to_1gpu_image": rel, "equal": bool(torch.equal(im, ref)), "ok": rel <= 1e-6}
+            # T11: 1e-5, the fp32 order of chirp-chunk sums (legs split their chirps
+            # differently; every pixel's anchor and derived-leg grouping are the same)
+            check[name] = {"max_rel_diff_to_1gpu_image": rel, "equal": bool(torch.equal(im, ref)), "ok": rel <= 1e-5}
         flags = torch.tensor([0 if c["ok"] else 1 for c in check.values()], device=dev)
         dist.all_reduce(flags, op=dist.ReduceOp.MAX)   # every rank agrees on the verdict
         for name, bad in zip(check, flags.tolist()):
@@ -386,15 +392,15 @@ def run_ours(args):
         del ref
     else:
         check["nccl"] = {"ok": True}
-    gather = gather_summary(world, legs, check) if world > 1 else None
-    head = "nccl" if world == 1 else gather["headline"]
+    gather = gather_summary(world, legs, check) if dist_on else None
+    head = "nccl" if not dist_on else gather["headline"]
     if head is None:   # no leg produced the 1-GPU image: report the failure, no number
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "invalid":
                               "no gather leg reproduced the 1-GPU image", "gather": gather,
                               "config": config_dict(args, scn)}), flush=True)
         plan.close()
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return 1
     leg = legs[head]
@@ -482,7 +488,7 @@ def run_ours(args):
                          f"({res['t_bp_s']:.2f} s), full image extrapolated to {res['est_image_s']:.1f} s"}
 
     if rank == 0:
-        if world == 1:
+        if head == "nccl" and world == 1:
             par, step_txt = "pixel tiles x1", "sar_range_compress(all chirps) + sar_backproject(all rows)"
         elif head == "fused":
             par = (f"pixel tiles x{world} (balanced tile blocks) + gather fused into the BP epilogue "
@@ -516,7 +522,7 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     plan.close()
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 
@@ -653,6 +659,9 @@ def run_stream(args):
 
 
 def main(argv=None):
+    # the JSON line is the only stdout line: NCCL's version banner (NCCL_DEBUG=VERSION) would precede it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -662,6 +671,8 @@ def main(argv=None):
     ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--all-legs", action="store_true",
+                    help="N = 1 check run: a one-rank process group, both gather legs timed and checked")
     ap.add_argument("--gather", default="auto", choices=["auto", "fused", "multicast", "nccl"],
                     help="N > 1, image configs: besides the NCCL all_gather leg (always timed), time the gather "
                          "fused into the BP epilogue (auto/fused: P2P stores, multicast: multimem.st to the "

@@ -264,7 +264,9 @@ __device__ __forceinline__ void stockham_stage(float2* v, float2* row, const flo
 // contiguous 2 Ns floats per stage, mbarrier completion), so the transform of one pair overlaps
 // the HBM latency of the next ones.  RING = 0 reads the rows with plain loads (rows not 16-B
 // aligned, or raw samples in mapped host memory).
-template <int L, int WARPS, int RING>
+// FULL: Ns == L (every BASELINE config at Ns = 512 or 256): stage 0 reads every sample with
+// compile-time offsets, no clamp or zero select.
+template <int L, int WARPS, int RING, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_kernel_warp(const RcArgs a) {
   extern __shared__ __align__(16) float2 xs[];   // [zp][RS] | raw ring [RING][2 ns] | mbarriers
   constexpr int E = RcWarpPlan<L>::E, RS = RcWarpPlan<L>::RS;
@@ -318,12 +320,12 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int t = j + r * (L / 8);
-          const int tc = min(t, a.ns - 1);
+          const int tc = FULL ? t : min(t, a.ns - 1);
           const float2 c = __ldg(cb + tc);
           const float va = RING > 0 ? xa[tc] : __ldg(xa + tc);
           const float vb = has_b ? (RING > 0 ? xb[tc] : __ldg(xb + tc)) : 0.f;
           const float2 z = make_float2(c.x * va - c.y * vb, c.x * vb + c.y * va);
-          v[r] = t < a.ns ? z : make_float2(0.f, 0.f);
+          v[r] = (FULL || t < a.ns) ? z : make_float2(0.f, 0.f);
         }
         dft<8>(v);
         float2* dst = row + 9 * j;                 // rpos(8 j + r) = 9 j + r
@@ -344,11 +346,27 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
     const float sb = a.scale * (a.wsar ? __ldg(a.wsar + mb) : 1.f);
     float2* pa = a.prof + (size_t)ra * a.n_bins;
     float2* pb = pa + a.n_bins;
-    for (int i = threadIdx.x; i < a.n_bins; i += WARPS * 32) {
+    // Z[k] for k = k_lo + i and its mirror Z[N - k]; stepping i by the block (a multiple of zp)
+    // keeps k mod zp and moves the row position by a constant: addresses advance linearly
+    // (the crop lies in [0, N/2 + 1], so N - k never wraps except at k = 0)
+    constexpr int kStep = WARPS * 32;
+    const int hk = a.k_lo + threadIdx.x;
+    const float2* zk = xs + (hk & (zp - 1)) * RS + rpos(hk >> lzp);
+    const int hn = (N - hk) & (N - 1);
+    const float2* zn = xs + (hn & (zp - 1)) * RS + rpos(hn >> lzp);
+    const int dstep = rpos(kStep >> lzp);   // row positions per block step (kStep / zp is a multiple of 8)
+    const bool lin = (kStep % zp) == 0 && ((kStep >> lzp) & 7) == 0 && a.k_lo > 0;
+    for (int i = threadIdx.x; i < a.n_bins; i += kStep, zk += dstep, zn -= dstep) {
       const int k = a.k_lo + i;
-      const int kn = (N - k) & (N - 1);
-      const float2 Zk = xs[(k & (zp - 1)) * RS + rpos(k >> lzp)];
-      const float2 Zn = xs[(kn & (zp - 1)) * RS + rpos(kn >> lzp)];
+      float2 Zk, Zn;
+      if (lin) {
+        Zk = *zk;
+        Zn = *zn;
+      } else {
+        const int kn = (N - k) & (N - 1);
+        Zk = xs[(k & (zp - 1)) * RS + rpos(k >> lzp)];
+        Zn = xs[(kn & (zp - 1)) * RS + rpos(kn >> lzp)];
+      }
       const float2 r = __ldg(a.ramp + i);
       const float2 A = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
       const float2 B = make_float2(0.5f * (Zk.y + Zn.y), -0.5f * (Zk.x - Zn.x));
@@ -366,9 +384,9 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
 #endif
 constexpr int kRcRing = SAR_RC_RING;
 
-template <int L, int WARPS, int RING>
+template <int L, int WARPS, int RING, bool FULL>
 cudaError_t launch_warp_ring(const RcArgs& a, cudaStream_t s) {
-  auto kern = rc_kernel_warp<L, WARPS, RING>;
+  auto kern = rc_kernel_warp<L, WARPS, RING, FULL>;
   const size_t smem = (size_t)(a.nfft / L) * RcWarpPlan<L>::RS * sizeof(float2) +
                       (RING > 0 ? (size_t)RING * (2 * a.ns * sizeof(float) + 8) : 0);
   // the opt-in is per device: set once to the largest plan this instantiation can see
@@ -397,10 +415,10 @@ cudaError_t launch_warp(const RcArgs& a, cudaStream_t s) {
   // bulk copies need 16-B aligned rows in device memory
   cudaPointerAttributes pa;
   const bool dev_mem = cudaPointerGetAttributes(&pa, a.raw) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
-  if (dev_mem && a.ns % 4 == 0 && (reinterpret_cast<uintptr_t>(a.raw) & 15) == 0)
-    return launch_warp_ring<L, WARPS, kRcRing>(a, s);
-  cudaGetLastError();   // clear a failed attribute query
-  return launch_warp_ring<L, WARPS, 0>(a, s);
+  const bool ring = dev_mem && a.ns % 4 == 0 && (reinterpret_cast<uintptr_t>(a.raw) & 15) == 0;
+  if (!dev_mem) cudaGetLastError();   // clear a failed attribute query
+  if (a.ns == L) return ring ? launch_warp_ring<L, WARPS, kRcRing, true>(a, s) : launch_warp_ring<L, WARPS, 0, true>(a, s);
+  return ring ? launch_warp_ring<L, WARPS, kRcRing, false>(a, s) : launch_warp_ring<L, WARPS, 0, false>(a, s);
 }
 
 }  // namespace
