@@ -203,8 +203,8 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
  *                               multimem.st / multimem.red reach every rank's image at once
  * With symmetric memory the images are the P2P-mapped buffers of every rank (one NVLink
  * store or reduction per peer).  Rows outside [row0, row0 + nrow) are not touched; the caller
- * orders the ranks (e.g. a symmetric-memory barrier) before reading.  A store scatter whose
- * shard cannot fill 7 waves of the GPU unsplit runs chirp-split: each chunk stores its partial
+ * orders the ranks (e.g. a symmetric-memory barrier) before reading.  A store scatter runs
+ * chirp-split (to about 16 waves of resident CTAs): each chunk stores its partial
  * tile into its own plane of a stream-ordered workspace from the plan's pool and the last chunk
  * of each tile sums the planes in chunk order and stores the finished tile (SAR_ERR_NO_MEMORY
  * never results: without the workspace it runs unsplit).  SAR_SCATTER_ADD runs unsplit; its

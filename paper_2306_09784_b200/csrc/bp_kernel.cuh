@@ -102,6 +102,16 @@ constexpr long kMinSplitItems = SAR_BP_MIN_SPLIT;
 #define SAR_BP_SPLIT_WAVES 32
 #endif
 constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
+// Scatter launches (the fused gather; sar_form_image's host-image stores) aim at 16 waves and never
+// run unsplit: measured on one GPU (tools/rank_probe2.py, tools/scatter_policy.sh), per-rank C3 tile
+// blocks N = 2: 28.44 ms unsplit (7.5 waves) -> 27.80 split; N = 8: 7.13 (32 waves) -> 7.09; C3 e2e
+// (host image) 56.62 -> 55.86 ms
+constexpr long kScatterWaves = 16;
+constexpr long kScatterUnsplit = 1L << 40;   // (a depth at which a scatter would run unsplit: none)
+inline long env_long(const char* name, long dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atol(e) : dflt;
+}
 // pixel (column x, image row y) inside the launch's image rows (y < 0: a tile row starting above)
 #define SAR_PIX_OK(x, y) ((x) < a.nx && (unsigned)(y) < (unsigned)a.nrow)
 #ifndef SAR_BP_RX_UNROLL
@@ -1077,14 +1087,16 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
   const long slots = (long)std::max(1, resident) * sms;
+  // scatters (tuning: SAR_BP_SCATTER_WAVES, SAR_BP_SCATTER_UNSPLIT): the split publish reads every
+  // chunk plane of a tile, so scatters aim at fewer waves than plain launches
+  static const long scatter_waves = env_long("SAR_BP_SCATTER_WAVES", kScatterWaves);
+  static const long scatter_unsplit = env_long("SAR_BP_SCATTER_UNSPLIT", kScatterUnsplit);
+  const long waves = a.n_peer > 0 ? scatter_waves : kSplitWaves;
   int k = 1;
-  while (ntiles * k < kSplitWaves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
+  while (ntiles * k < waves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
          a.nchirp / (2 * k) >= a.CB)
     k *= 2;
-  // scatters: unsplit when that already fills 7 waves.  Cost over the plain split launch,
-  // measured: unsplit +1.0 % at 7.5 waves (C3 rows / 2), +4 % at 6.0 (C2 to a host image),
-  // +5.9 % at 3.7 (C3 rows / 4); the split publish costs +2.4 %
-  if (a.n_peer > 0 && ntiles >= 7 * slots) k = 1;
+  if (a.n_peer > 0 && ntiles >= scatter_unsplit * slots) k = 1;
   // reductions into peers (chirp shards) run unsplit
   if (a.n_peer > 0 && a.accumulate) k = 1;
   auto split = [&](int kk) {

@@ -1003,7 +1003,7 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   if (st != SAR_OK) return st;
   // Image readback fused into the BP epilogue: when the host image is pinned (device-mapped
   // under UVA) every finished tile is stored straight into host memory while the other tiles
-  // compute (unsplit when that fills 7 waves, else under a chirp split by the last chunk of
+  // compute (under a chirp split by the last chunk of
   // each tile from an accumulation image);
   // else one device->host copy after the kernel.
   void* mapped = nullptr;
