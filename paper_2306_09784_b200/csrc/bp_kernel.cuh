@@ -58,6 +58,9 @@ namespace sar {
 namespace {
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+#ifndef SAR_BP_NRX_SPEC
+#define SAR_BP_NRX_SPEC 0   // derived bistatic stages with a compile-time count of 4 RX (tuning)
+#endif
 #ifndef SAR_BP_GROUP
 #define SAR_BP_GROUP 8
 #endif
@@ -781,25 +784,39 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const f32x2 P = ffma2(D, ffma2(D, ffma2(D, bc2(-0.0390625f), bc2(0.0625f)), bc2(-0.125f)), bc2(0.5f));
           return ffma2(EQ, P, base);
         };
+        auto stage = [&](auto nrx_tag) {   // NRX > 0: the RX count at compile time
+          constexpr int NRX = decltype(nrx_tag)::value;
 #pragma unroll 1
-        for (int c = 0; c < cnt; ++c) {
-          f32x2 TS[PB / 2];
-          if (c == 0) {
+          for (int c = 0; c < cnt; ++c) {
+            f32x2 TS[PB / 2];
+            if (c == 0) {
 #pragma unroll
-            for (int h = 0; h < PB / 2; ++h) TS[h] = DR2[h];
-          } else {
-            const float4 T = srec[2 * c];
+              for (int h = 0; h < PB / 2; ++h) TS[h] = DR2[h];
+            } else {
+              const float4 T = srec[2 * c];
 #pragma unroll
-            for (int h = 0; h < PB / 2; ++h) TS[h] = xleg(T, h, DR2[h]);
-          }
-          const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
+              for (int h = 0; h < PB / 2; ++h) TS[h] = xleg(T, h, DR2[h]);
+            }
+            const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
+            if constexpr (NRX > 0) {
+#pragma unroll
+              for (int n = 0; n < NRX; ++n, rp += 2) {
+                const float4 A = rp[0], B = rp[1];
+#pragma unroll
+                for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+              }
+            } else {
 #pragma unroll kRxUnroll
-          for (int n = 0; n < a.n_rx; ++n, rp += 2) {
-            const float4 A = rp[0], B = rp[1];
+              for (int n = 0; n < a.n_rx; ++n, rp += 2) {
+                const float4 A = rp[0], B = rp[1];
 #pragma unroll
-            for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+                for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+              }
+            }
           }
-        }
+        };
+        if (SAR_BP_NRX_SPEC && a.n_rx == 4) stage(std::integral_constant<int, 4>{});
+        else stage(std::integral_constant<int, 0>{});
       } else {
 #pragma unroll 1
         for (int c = 0; c < cnt; ++c) {
@@ -808,13 +825,8 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 #pragma unroll
           for (int h = 0; h < PB / 2; ++h) DT[h] = leg_delta2(T, UX[h], UY[h], W2[h]);
           const float4* rp = srec + 2 * (a.CB + c * a.n_rx);
-#ifdef SAR_BP_EXP_NRX
-#pragma unroll
-          for (int n = 0; n < SAR_BP_EXP_NRX; ++n, rp += 2) {
-#else
 #pragma unroll kRxUnroll
           for (int n = 0; n < a.n_rx; ++n, rp += 2) {
-#endif
             const float4 A = rp[0], B = rp[1];
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h)
@@ -1044,10 +1056,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, mono_min_blocks(NCW, PB)) bp_k
   bp_body<false, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
-#ifndef SAR_BP_EXP_BI_MINB
-#define SAR_BP_EXP_BI_MINB 4
+#ifndef SAR_BP_BI_MINB
+#define SAR_BP_BI_MINB 4
 #endif
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? SAR_BP_EXP_BI_MINB : 1) bp_kernel_bi(const BpArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? SAR_BP_BI_MINB : 1) bp_kernel_bi(const BpArgs a) {
   bp_body<true, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool BI, bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
