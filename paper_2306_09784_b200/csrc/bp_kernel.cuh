@@ -77,12 +77,25 @@ constexpr int kJUnroll = SAR_BP_JUNROLL;
 #endif
 constexpr bool kDeriveMono = SAR_BP_DERIVE_MONO;   // derived-chirp groups compiled in (monostatic)
 constexpr bool kDeriveBi = SAR_BP_DERIVE_BI;       // derived stages compiled in (bistatic)
-// Series bounds |delta| of derived legs: truncation error <= 5 R delta^4 / 128 (3 terms,
-// monostatic groups) and 7 R delta^5 / 256 (4 terms, bistatic stages), below 1.6e-10 m at R >= 1 m
-// (< 1e-6 rad of carrier phase per update: the images stay within fp32 summation order of the
-// per-chirp rsqrt form, whatever the chirp order)
-constexpr double kDeriveDelta = 0.008;
-constexpr double kDeriveDeltaBi = 0.023;
+// Derived legs (reading A22): R sqrt(1 + delta) - R by the binomial series truncated after t
+// terms; the Taylor remainder bounds the truncation by R |delta|^(t+1) c_t (1 - |delta|)^-(t+1/2)
+// with c_2 = 1/16, c_3 = 5/128, c_4 = 7/256.  A group (stage) takes the fewest terms whose bound,
+// evaluated in fp64 over the whole tile (R <= r_b + rho_T + |o|), stays below kTruncMax; with
+// none, every leg keeps its own rsqrt.  kTruncMax = 1e-9 m is ~3e-6 rad of carrier phase per
+// update, 10x below the fp32 rounding of a leg (~1e-8 m).
+constexpr double kTruncMax = 1e-9;
+constexpr double kDeltaMax = 0.05;   // (and |delta| small enough that the remainder factor is ~1)
+// fewest series terms (2..tmax) of a leg with |delta| <= dl at range <= R; 99: not derivable
+__device__ __forceinline__ int series_terms(double dl, double R, int tmin, int tmax) {
+  if (!(dl >= 0.0 && dl <= kDeltaMax)) return 99;
+  const double f = 1.0 / (1.0 - dl);
+  double p = R * dl * dl * dl * f * f * sqrt(f);   // R dl^3 (1 - dl)^-2.5
+  const double c[3] = {1.0 / 16.0, 5.0 / 128.0, 7.0 / 256.0};
+  for (int t = 2; t <= 4; ++t, p *= dl * f) {
+    if (t >= tmin && t <= tmax && c[t - 2] * p <= kTruncMax) return t;
+  }
+  return 99;
+}
 constexpr uint32_t kMagicBits = 0x4B400000u;
 constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
 #ifndef SAR_BP_BATCH
@@ -482,12 +495,12 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         // RX legs -- follows from chirp 0's TX leg (the stage base b) by the series of the
         // monostatic groups, with o = q_leg - q_tx(b) (RX offsets included), so the consumers
         // spend one rsqrt per pixel per stage.  Records: TX of chirp c >= 1 and every RX item
-        // {-2 o_x, -2 o_y, -2 D_b.o + |o|^2, -}; RX anchor indices at 2 r_b (windows their own).
-        // Bound per leg (4-term series): (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 <= kDeriveDeltaBi.
-        volatile int* gflag = reinterpret_cast<volatile int*>(smem + L.flags);
-        __syncwarp();   // the stage's records (other lanes) are complete
-        if (lane == 0) gflag[0] = 1;
-        __syncwarp();
+        // {-2 o_x, -2 o_y, -2 D_b.o + |o|^2, -}.  Series terms (3 or 4) per stage: the most any
+        // leg needs, |delta| <= (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 (series_terms).
+        // Anchor indices: every RX leg's at 2 r_b (windows their own), split as
+        // kappa_b - 1/2 = n + phi with n an integer: the record holds n - k0 - W/2 + 1.5 2^23
+        // (exact in fp32) and the base record the fraction eps = phi / A1 (metres), which the
+        // consumers add to the base leg, so that the rounding of the index is one FFMA2.
         const Q3 qb = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0), a);
         const double Dbx = PTx - qb.x, Dby = PTy - qb.y, Dbz = PTz - qb.z;
         const double rb = sqrt(Dbx * Dbx + Dby * Dby + Dbz * Dbz), rmin = rb - rho_t;
@@ -498,14 +511,19 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           oy = q.y - qb.y;
           oz = q.z - qb.z;
         };
+        int tneed = 2;
         for (int k = lane; k < items + cnt; k += 32) {
           double ox, oy, oz;
           leg_o(k, ox, oy, oz);
           const double on = sqrt(ox * ox + oy * oy + oz * oz);
-          if (!(rmin > 0.0 && (2.0 * (rb + rho_t) * on + on * on) <= kDeriveDeltaBi * rmin * rmin)) gflag[0] = 0;
+          const double dl = rmin > 0.0 ? (2.0 * (rb + rho_t) * on + on * on) / (rmin * rmin) : -1.0;
+          tneed = max(tneed, series_terms(dl, rb + rho_t + on, 3, 4));
         }
-        __syncwarp();
-        if (gflag[0]) {
+        tneed = __reduce_max_sync(0xffffffffu, tneed);
+        __syncwarp();   // the stage's records (other lanes) are complete
+        if (tneed <= 4) {
+          const double kb = a.a1 * 2.0 * rb - a.k_lo - 0.5, nb = floor(kb);
+          const int wh = a.W >> 1;
           for (int k = lane; k < items + cnt; k += 32) {
             if (k == items) continue;   // chirp 0's TX leg stays the base leg
             double ox, oy, oz;
@@ -514,13 +532,15 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             const float4 rec_o = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
             if (k < items) {
               srec[2 * (a.CB + k)] = rec_o;
-              const int k0 = skw[k].x, wh = a.W >> 1;
-              srec[2 * (a.CB + k) + 1].x = (float)(a.a1 * 2.0 * rb - a.k_lo - k0 - 0.5 - wh);
+              srec[2 * (a.CB + k) + 1].x = (float)(nb - skw[k].x - wh + (double)kMagic);
             } else {
               srec[2 * (k - items)] = rec_o;
             }
           }
-          if (lane == 0) srec[1].w = 1.f;   // chirp 0's TX record: the stage is derived
+          if (lane == 0) {   // chirp 0's TX record: the stage is derived with tneed terms
+            srec[1].z = (float)((kb - nb) / (double)a.A1f);
+            srec[1].w = (float)tneed;
+          }
         }
         __syncwarp();
       }
@@ -532,16 +552,19 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         // so the consumers spend one rsqrt per pixel per group instead of per chirp.  The record
         // of a derived chirp is {-2 o_x, -2 o_y, c = -2 D_b.o + |o|^2 (fp64 -> fp32), -} and its
         // anchor index is taken at the base's anchor distance (its window start is its own).  A
-        // group is derived only when the series bound holds over the whole tile:
-        //   |delta| <= (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 <= kDeriveDelta
-        // (any track, any chirp order: otherwise every chirp of the group keeps its own leg).
+        // group is derived only when the series bound holds over the whole tile with 2 or 3 terms
+        // (series_terms), |delta| <= (2 (r_b + rho_T) |o| + |o|^2) / (r_b - rho_T)^2 (any track,
+        // any chirp order: otherwise every chirp of the group keeps its own leg).  As in the
+        // bistatic stages, the group's anchor indices are integers + 1.5 2^23 and the base record
+        // carries the fraction eps = phi / A1 (z) and the series terms (w).
         __syncwarp();
+        const int wh = a.W >> 1;
         for (int e0 = 0; e0 < items; e0 += 32) {
           const int c = e0 + lane;
           const int cb = c - (c % kGroup);
-          bool ok = c < cnt && cb + kGroup <= cnt;
+          int t = 99;
           double ox = 0, oy = 0, oz = 0, Dbx = 0, Dby = 0, Dbz = 0, rb = 0;
-          if (ok) {
+          if (c < cnt && cb + kGroup <= cnt) {
             const Q3 qj = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0 + c), a);
             const Q3 qb = ld_pos(a.tx + 3 * (size_t)(chirp0 + c0 + cb), a);
             ox = qj.x - qb.x;
@@ -552,18 +575,21 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             Dbz = PTz - qb.z;
             rb = sqrt(Dbx * Dbx + Dby * Dby + Dbz * Dbz);
             const double on = sqrt(ox * ox + oy * oy + oz * oz), rmin = rb - rho_t;
-            ok = rmin > 0.0 && (2.0 * (rb + rho_t) * on + on * on) <= kDeriveDelta * rmin * rmin;
+            if (rmin > 0.0) t = series_terms((2.0 * (rb + rho_t) * on + on * on) / (rmin * rmin), rb + rho_t + on, 2, 3);
           }
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
-          const bool grp = ((bal >> (lane & ~(kGroup - 1))) & ((1u << kGroup) - 1)) == ((1u << kGroup) - 1);
-          if (c < cnt && grp) {
-            if (c == cb) {
-              srec[2 * c + 1].w = 1.f;   // base record: the group is derived
+          // the group's terms: the most any of its kGroup lanes needs
+          int tg = t;
+#pragma unroll
+          for (int s = 1; s < kGroup; s <<= 1) tg = max(tg, __shfl_xor_sync(0xffffffffu, tg, s));
+          if (c < cnt && tg <= 3) {
+            const double kb = a.a1 * 2.0 * rb - a.k_lo - 0.5, nb = floor(kb);
+            srec[2 * c + 1].x = (float)(nb - skw[c].x - wh + (double)kMagic);
+            if (c == cb) {   // base record: the group is derived with tg terms
+              srec[2 * c + 1].z = (float)((kb - nb) / (double)a.A1f);
+              srec[2 * c + 1].w = (float)tg;
             } else {
               const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
               srec[2 * c] = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
-              const int k0 = skw[c].x, wh = a.W >> 1;
-              srec[2 * c + 1].x = (float)(a.a1 * 2.0 * rb - a.k_lo - k0 - 0.5 - wh);
             }
           }
         }
@@ -713,11 +739,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
       // v exp(j th) = vr (cs, sn) + vi (-sn, cs): the two halves go to separate accumulators,
       // ACC += vr (cs, sn) and ACI += vi (sn, cs) (a swizzle, no negation); the epilogue
       // forms (ACC.re - ACI.re, ACC.im + ACI.im).
-      auto tail = [&](const int h, const f32x2 DR, const float kap_a, const uint32_t off) {
-        f32x2 KAP = ffma2(bc2(A1), DR, bc2(kap_a));                                   // Alg. 2 L8
-        if (DOP) KAP = fadd2(KAP, FD2[h]);
-        const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
-        const f32x2 GF = fsub2(KAP, fsub2(TK, bc2(kMagic)));                        // gf in [-1/2, 1/2]
+      // tail_core: TK = 1.5 2^23 + round(kappa) (its bits address the window entry), GF = kappa -
+      // round(kappa) in [-1/2, 1/2]
+      auto tail_core = [&](const int h, const f32x2 TK, const f32x2 GF, const uint32_t off) {
         const f32x2 TH = fmul2(GF, bc2(C3));                                        // 2 pi beta gf
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -734,31 +758,57 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           ACI[2 * h + k] = ffma2(bc2(hi2(V)), pk2(sn, cs), ACI[2 * h + k]);
         }
       };
+      // tail: the leg's own anchor index kap_a (fractional)                       Alg. 2 L8
+      auto tail = [&](const int h, const f32x2 DR, const float kap_a, const uint32_t off) {
+        f32x2 KAP = ffma2(bc2(A1), DR, bc2(kap_a));
+        if (DOP) KAP = fadd2(KAP, FD2[h]);
+        const f32x2 TK = fadd2(KAP, bc2(kMagic));                                   // round
+        tail_core(h, TK, fsub2(KAP, fsub2(TK, bc2(kMagic))), off);
+      };
+      // tail_n: derived legs, whose DR carries the anchor's fraction (eps) and whose record holds
+      // the integer rest nM = n + 1.5 2^23: TK = A1 DR + nM is the rounding, nM - TK is exact
+      auto tail_n = [&](const int h, const f32x2 DR, const float nM, const uint32_t off) {
+        if (DOP) {
+          const f32x2 KF = ffma2(bc2(A1), DR, FD2[h]);
+          const f32x2 TK = fadd2(KF, bc2(nM));
+          tail_core(h, TK, fadd2(KF, fsub2(bc2(nM), TK)), off);
+        } else {
+          const f32x2 TK = ffma2(bc2(A1), DR, bc2(nM));
+          tail_core(h, TK, ffma2(bc2(A1), DR, fsub2(bc2(nM), TK)), off);
+        }
+      };
       if (!BISTATIC) {
         for (int c = 0; c < cnt;) {
           const float4 A = srec[2 * c], B = srec[2 * c + 1];
           if (kDeriveMono && B.w != 0.f) {
-            // derived group (warp-uniform: one record for all): the base chirp's leg, then the
-            // kGroup - 1 others by the series  |p - q_j| - r_b = dR_b + (E Q) P(delta),
-            // delta = E Q^2 (Q = 1/R_b), P = 1/2 - delta/8 + delta^2/16  (truncation 5 delta^4 / 128)
+            // derived group (warp-uniform: one record for all): the base chirp's leg (plus the
+            // anchor fraction eps = B.z), then the kGroup - 1 others by the series
+            //   |p - q_j| - r_b = dR_b + (E Q) P(delta),  delta = E Q^2 (Q = 1/R_b),
+            //   P = 1/2 - delta/8 (+ delta^2/16 with 3 terms, B.w = 3)
             f32x2 DR0[PB / 2], Q0[PB / 2];
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h) {
-              DR0[h] = leg_delta2q(A, UX[h], UY[h], W2[h], Q0[h]);
-              tail(h, DR0[h], B.x, __float_as_uint(B.y));
+              DR0[h] = fadd2(leg_delta2q(A, UX[h], UY[h], W2[h], Q0[h]), bc2(B.z));
+              tail_n(h, DR0[h], B.x, __float_as_uint(B.y));
             }
+            auto group = [&](auto terms_tag) {
+              constexpr int TERMS = decltype(terms_tag)::value;
 #pragma unroll kJUnroll
-            for (int j = 1; j < kGroup; ++j) {
-              const float4 Aj = srec[2 * (c + j)], Bj = srec[2 * (c + j) + 1];
+              for (int j = 1; j < kGroup; ++j) {
+                const float4 Aj = srec[2 * (c + j)], Bj = srec[2 * (c + j) + 1];
 #pragma unroll
-              for (int h = 0; h < PB / 2; ++h) {
-                const f32x2 E = ffma2(bc2(Aj.x), UX[h], ffma2(bc2(Aj.y), UY[h], bc2(Aj.z)));
-                const f32x2 EQ = fmul2(E, Q0[h]);      // ~ R_b delta
-                const f32x2 D = fmul2(EQ, Q0[h]);      // delta
-                const f32x2 P = ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f));
-                tail(h, ffma2(EQ, P, DR0[h]), Bj.x, __float_as_uint(Bj.y));
+                for (int h = 0; h < PB / 2; ++h) {
+                  const f32x2 E = ffma2(bc2(Aj.x), UX[h], ffma2(bc2(Aj.y), UY[h], bc2(Aj.z)));
+                  const f32x2 EQ = fmul2(E, Q0[h]);      // ~ R_b delta
+                  const f32x2 D = fmul2(EQ, Q0[h]);      // delta
+                  const f32x2 P = TERMS == 2 ? ffma2(D, bc2(-0.125f), bc2(0.5f))
+                                             : ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f));
+                  tail_n(h, ffma2(EQ, P, DR0[h]), Bj.x, __float_as_uint(Bj.y));
+                }
               }
-            }
+            };
+            if (B.w == 2.f) group(std::integral_constant<int, 2>{});
+            else group(std::integral_constant<int, 3>{});
             c += kGroup;
           } else {
 #pragma unroll
@@ -770,22 +820,26 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
         // derived stage (bistatic): chirp 0's TX leg by rsqrt; every other leg l of the stage by
         // |p - q_l| - r_b = dR_b + (E Q) P4(delta), delta = E Q^2,
         // P4 = 1/2 - delta/8 + delta^2/16 - 5 delta^3/128; d_hyp - 2 r_b = 2 dR_b + X_tx + X_rx
-        const float4 T0 = srec[0];
+        // (3-term stages: P3 = 1/2 - delta/8 + delta^2/16; srec[1].w = terms, srec[1].z = eps)
+        const float4 T0 = srec[0], T0b = srec[1];
         f32x2 DR2[PB / 2], Q0[PB / 2];
 #pragma unroll
         for (int h = 0; h < PB / 2; ++h) {
           const f32x2 d0 = leg_delta2q(T0, UX[h], UY[h], W2[h], Q0[h]);
-          DR2[h] = fadd2(d0, d0);
+          DR2[h] = ffma2(d0, bc2(2.f), bc2(T0b.z));   // 2 dR_b + eps
         }
-        auto xleg = [&](const float4 R, const int h, const f32x2 base) {   // base + (E Q) P4(delta), leg of record R
-          const f32x2 E = ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
-          const f32x2 EQ = fmul2(E, Q0[h]);
-          const f32x2 D = fmul2(EQ, Q0[h]);
-          const f32x2 P = ffma2(D, ffma2(D, ffma2(D, bc2(-0.0390625f), bc2(0.0625f)), bc2(-0.125f)), bc2(0.5f));
-          return ffma2(EQ, P, base);
-        };
-        auto stage = [&](auto nrx_tag) {   // NRX > 0: the RX count at compile time
+        auto stage = [&](auto nrx_tag, auto terms_tag) {   // NRX > 0: the RX count at compile time
           constexpr int NRX = decltype(nrx_tag)::value;
+          constexpr int TERMS = decltype(terms_tag)::value;
+          auto xleg = [&](const float4 R, const int h, const f32x2 base) {   // base + (E Q) P(delta), leg of record R
+            const f32x2 E = ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
+            const f32x2 EQ = fmul2(E, Q0[h]);
+            const f32x2 D = fmul2(EQ, Q0[h]);
+            const f32x2 P = TERMS == 3
+                                ? ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f))
+                                : ffma2(D, ffma2(D, ffma2(D, bc2(-0.0390625f), bc2(0.0625f)), bc2(-0.125f)), bc2(0.5f));
+            return ffma2(EQ, P, base);
+          };
 #pragma unroll 1
           for (int c = 0; c < cnt; ++c) {
             f32x2 TS[PB / 2];
@@ -803,20 +857,25 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
               for (int n = 0; n < NRX; ++n, rp += 2) {
                 const float4 A = rp[0], B = rp[1];
 #pragma unroll
-                for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+                for (int h = 0; h < PB / 2; ++h) tail_n(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
               }
             } else {
 #pragma unroll kRxUnroll
               for (int n = 0; n < a.n_rx; ++n, rp += 2) {
                 const float4 A = rp[0], B = rp[1];
 #pragma unroll
-                for (int h = 0; h < PB / 2; ++h) tail(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
+                for (int h = 0; h < PB / 2; ++h) tail_n(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
               }
             }
           }
         };
-        if (SAR_BP_NRX_SPEC && a.n_rx == 4) stage(std::integral_constant<int, 4>{});
-        else stage(std::integral_constant<int, 0>{});
+        if (SAR_BP_NRX_SPEC && a.n_rx == 4) {
+          if (T0b.w == 3.f) stage(std::integral_constant<int, 4>{}, std::integral_constant<int, 3>{});
+          else stage(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+        } else {
+          if (T0b.w == 3.f) stage(std::integral_constant<int, 0>{}, std::integral_constant<int, 3>{});
+          else stage(std::integral_constant<int, 0>{}, std::integral_constant<int, 4>{});
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < cnt; ++c) {

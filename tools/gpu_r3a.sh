@@ -1,0 +1,5 @@
+# round-2 session 3: integer-index tails + adaptive series terms (A/B against the previous build)
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -5
+bash tools/gpu_sweep.sh "C3 C0 C2" tools/ab/libsar_base.so tools/ab/libsar_int.so
+bash tools/gpu_shard_sweep.sh C4 750 750 tools/ab/libsar_base.so tools/ab/libsar_int.so
