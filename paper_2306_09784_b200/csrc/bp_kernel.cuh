@@ -75,6 +75,24 @@ constexpr int kJUnroll = SAR_BP_JUNROLL;
 #ifndef SAR_BP_DERIVE_BI
 #define SAR_BP_DERIVE_BI 1
 #endif
+#ifndef SAR_BP_COL_MONO
+// collinear monostatic groups (tuning switch): fewer FFMA2 per derived chirp, but the extra
+// group variants cost registers and spills -- measured slower on C0/C2 (straight) and C3
+// (9.42 -> 9.86, 21.50 -> 22.04, 52.13 -> 52.93 ms); the bistatic stages keep them (C4 -2 %)
+#define SAR_BP_COL_MONO 0
+#endif
+constexpr bool kColMono = SAR_BP_COL_MONO;
+#ifndef SAR_BP_HORNER
+// derived legs in Horner form in E: R_b (sqrt(1 + E Q^2) - 1) = E (Q/2 + E (-Q^3/8 + E (Q^5/16 ..)))
+// with the coefficients formed once per group / stage (one FFMA2 per term instead of E Q, delta,
+// P(delta), EQ P)
+#define SAR_BP_HORNER 1
+#endif
+#ifndef SAR_BP_HORNER_MAX
+#define SAR_BP_HORNER_MAX 2   // Horner form for series of at most this many terms (measured: 2 -> C3 -0.6 %; 3-4 term Horner variants cost registers: C3 +1.9 %, C4 shard +0 to +19 %)
+#endif
+constexpr bool kHorner = SAR_BP_HORNER;
+constexpr int kHornerMax = SAR_BP_HORNER_MAX;
 constexpr bool kDeriveMono = SAR_BP_DERIVE_MONO;   // derived-chirp groups compiled in (monostatic)
 constexpr bool kDeriveBi = SAR_BP_DERIVE_BI;       // derived stages compiled in (bistatic)
 // Derived legs (reading A22): R sqrt(1 + delta) - R by the binomial series truncated after t
@@ -95,6 +113,32 @@ __device__ __forceinline__ int series_terms(double dl, double R, int tmin, int t
     if (t >= tmin && t <= tmax && c[t - 2] * p <= kTruncMax) return t;
   }
   return 99;
+}
+// Collinear legs: pixels lie in the plane z = z0, so a leg's offset o enters the per-pixel part of
+// E = -2 (D_b + u).o + |o|^2 through its horizontal part only.  When every horizontal offset of a
+// group (stage) lies along one unit direction e -- a straight track, an array along it -- then
+// o_h.u = (o_h.e)(e.u) and the consumers spend one FFMA2 on E (e.u formed once per group).  The
+// dropped perpendicular part changes a leg by <= |o_perp| rho_T / (r_b - rho_T): a group is
+// collinear when that stays below kTruncMax / 10.
+// group_dir: e = direction of the largest horizontal offset among `width` aligned lanes (xor
+// butterfly, ties broken lexicographically so that every lane ends with the same vector).
+__device__ __forceinline__ void group_dir(double ox, double oy, int width, double& ex, double& ey) {
+  double n = ox * ox + oy * oy, bx = ox, by = oy;
+  for (int s = 1; s < width; s <<= 1) {
+    const double n2 = __shfl_xor_sync(0xffffffffu, n, s), x2 = __shfl_xor_sync(0xffffffffu, bx, s),
+                 y2 = __shfl_xor_sync(0xffffffffu, by, s);
+    if (n2 > n || (n2 == n && (x2 > bx || (x2 == bx && y2 > by)))) {
+      n = n2;
+      bx = x2;
+      by = y2;
+    }
+  }
+  const double len = sqrt(n);
+  ex = len > 0.0 ? bx / len : 1.0;
+  ey = len > 0.0 ? by / len : 0.0;
+}
+__device__ __forceinline__ bool leg_collinear(double ox, double oy, double ex, double ey, double rho, double rmin) {
+  return fabs(ox * ey - oy * ex) * rho <= 0.1 * kTruncMax * rmin;
 }
 constexpr uint32_t kMagicBits = 0x4B400000u;
 constexpr int kPatchX = 8, kPatchY = 4;  // pixel patch of one warp for one register slot
@@ -234,6 +278,24 @@ __device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
   return d;
 }
 __device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
+
+// Horner coefficients of the series, Q ~ 1/R_b: H[0] = Q/2, H[1] = -Q^3/8, H[2] = Q^5/16, H[3] = -5 Q^7/128
+template <int TERMS>
+__device__ __forceinline__ void horner_coef(const f32x2 Q, f32x2* H) {
+  const f32x2 Q2 = fmul2(Q, Q);
+  H[0] = fmul2(Q, bc2(0.5f));
+  H[1] = fmul2(fmul2(Q2, Q), bc2(-0.125f));
+  if (TERMS >= 3) H[2] = fmul2(fmul2(Q2, H[1]), bc2(-0.5f));
+  if (TERMS >= 4) H[3] = fmul2(fmul2(Q2, H[2]), bc2(-0.625f));
+}
+// base + E (H0 + E (H1 + E (H2 + E H3)))
+template <int TERMS>
+__device__ __forceinline__ f32x2 horner_leg(const f32x2 E, const f32x2* H, const f32x2 base) {
+  f32x2 t = H[TERMS - 1];
+#pragma unroll
+  for (int k = TERMS - 2; k >= 0; --k) t = ffma2(E, t, H[k]);
+  return ffma2(E, t, base);
+}
 
 __device__ __forceinline__ float rsqrt_mufu(float x) {
   float y;
@@ -512,14 +574,28 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           oz = q.z - qb.z;
         };
         int tneed = 2;
+        double mx = 0.0, my = 0.0;   // this lane's largest horizontal offset
         for (int k = lane; k < items + cnt; k += 32) {
           double ox, oy, oz;
           leg_o(k, ox, oy, oz);
           const double on = sqrt(ox * ox + oy * oy + oz * oz);
           const double dl = rmin > 0.0 ? (2.0 * (rb + rho_t) * on + on * on) / (rmin * rmin) : -1.0;
           tneed = max(tneed, series_terms(dl, rb + rho_t + on, 3, 4));
+          if (ox * ox + oy * oy > mx * mx + my * my) {
+            mx = ox;
+            my = oy;
+          }
         }
         tneed = __reduce_max_sync(0xffffffffu, tneed);
+        double ex, ey;
+        group_dir(mx, my, 32, ex, ey);
+        bool col = true;
+        for (int k = lane; k < items + cnt; k += 32) {
+          double ox, oy, oz;
+          leg_o(k, ox, oy, oz);
+          col = col && leg_collinear(ox, oy, ex, ey, rho_t, rmin);
+        }
+        col = __all_sync(0xffffffffu, col);
         __syncwarp();   // the stage's records (other lanes) are complete
         if (tneed <= 4) {
           const double kb = a.a1 * 2.0 * rb - a.k_lo - 0.5, nb = floor(kb);
@@ -529,7 +605,8 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             double ox, oy, oz;
             leg_o(k, ox, oy, oz);
             const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
-            const float4 rec_o = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
+            const float4 rec_o = col ? make_float4((float)(-2.0 * (ox * ex + oy * ey)), 0.f, (float)cj, 0.f)
+                                     : make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
             if (k < items) {
               srec[2 * (a.CB + k)] = rec_o;
               srec[2 * (a.CB + k) + 1].x = (float)(nb - skw[k].x - wh + (double)kMagic);
@@ -537,10 +614,8 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
               srec[2 * (k - items)] = rec_o;
             }
           }
-          if (lane == 0) {   // chirp 0's TX record: the stage is derived with tneed terms
-            srec[1].z = (float)((kb - nb) / (double)a.A1f);
-            srec[1].w = (float)tneed;
-          }
+          if (lane == 0)   // chirp 0's TX record: {e, eps, terms (+ 16: collinear)}
+            srec[1] = make_float4((float)ex, (float)ey, (float)((kb - nb) / (double)a.A1f), (float)(tneed + (col ? 16 : 0)));
         }
         __syncwarp();
       }
@@ -581,15 +656,26 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           int tg = t;
 #pragma unroll
           for (int s = 1; s < kGroup; s <<= 1) tg = max(tg, __shfl_xor_sync(0xffffffffu, tg, s));
+          // collinear group (e from the group's largest offset; records 1 and 2 carry e in w)
+          double ex = 1.0, ey = 0.0;
+          bool col = false;
+          if constexpr (kColMono) {
+            group_dir(ox, oy, kGroup, ex, ey);
+            const unsigned cbal = __ballot_sync(0xffffffffu, leg_collinear(ox, oy, ex, ey, rho_t, rb - rho_t));
+            col = ((cbal >> (lane & ~(kGroup - 1))) & ((1u << kGroup) - 1)) == ((1u << kGroup) - 1);
+          }
           if (c < cnt && tg <= 3) {
             const double kb = a.a1 * 2.0 * rb - a.k_lo - 0.5, nb = floor(kb);
             srec[2 * c + 1].x = (float)(nb - skw[c].x - wh + (double)kMagic);
-            if (c == cb) {   // base record: the group is derived with tg terms
+            if (c == cb) {   // base record: the group is derived with tg terms (+ 4: collinear)
               srec[2 * c + 1].z = (float)((kb - nb) / (double)a.A1f);
-              srec[2 * c + 1].w = (float)tg;
+              srec[2 * c + 1].w = (float)(tg + (col ? 4 : 0));
             } else {
               const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
-              srec[2 * c] = make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
+              const int j = c - cb;
+              srec[2 * c] = col ? make_float4((float)(-2.0 * (ox * ex + oy * ey)), 0.f, (float)cj,
+                                              j == 1 ? (float)ex : j == 2 ? (float)ey : 0.f)
+                                : make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
             }
           }
         }
@@ -791,24 +877,46 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
               DR0[h] = fadd2(leg_delta2q(A, UX[h], UY[h], W2[h], Q0[h]), bc2(B.z));
               tail_n(h, DR0[h], B.x, __float_as_uint(B.y));
             }
-            auto group = [&](auto terms_tag) {
+            auto group = [&](auto terms_tag, auto col_tag) {
               constexpr int TERMS = decltype(terms_tag)::value;
+              constexpr bool COL = decltype(col_tag)::value;   // collinear: E = c + s (e.u)
+              f32x2 UE[PB / 2];
+              if (COL) {
+                const float ex = srec[2 * (c + 1)].w, ey = srec[2 * (c + 2)].w;
+#pragma unroll
+                for (int h = 0; h < PB / 2; ++h) UE[h] = ffma2(bc2(ex), UX[h], fmul2(bc2(ey), UY[h]));
+              }
+              constexpr bool HORN = kHorner && TERMS <= kHornerMax;
+              f32x2 H[PB / 2][TERMS];
+              if (HORN) {
+#pragma unroll
+                for (int h = 0; h < PB / 2; ++h) horner_coef<TERMS>(Q0[h], H[h]);
+              }
 #pragma unroll kJUnroll
               for (int j = 1; j < kGroup; ++j) {
                 const float4 Aj = srec[2 * (c + j)], Bj = srec[2 * (c + j) + 1];
 #pragma unroll
                 for (int h = 0; h < PB / 2; ++h) {
-                  const f32x2 E = ffma2(bc2(Aj.x), UX[h], ffma2(bc2(Aj.y), UY[h], bc2(Aj.z)));
-                  const f32x2 EQ = fmul2(E, Q0[h]);      // ~ R_b delta
-                  const f32x2 D = fmul2(EQ, Q0[h]);      // delta
-                  const f32x2 P = TERMS == 2 ? ffma2(D, bc2(-0.125f), bc2(0.5f))
-                                             : ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f));
-                  tail_n(h, ffma2(EQ, P, DR0[h]), Bj.x, __float_as_uint(Bj.y));
+                  const f32x2 E = COL ? ffma2(bc2(Aj.x), UE[h], bc2(Aj.z))
+                                      : ffma2(bc2(Aj.x), UX[h], ffma2(bc2(Aj.y), UY[h], bc2(Aj.z)));
+                  if (HORN) {
+                    tail_n(h, horner_leg<TERMS>(E, H[h], DR0[h]), Bj.x, __float_as_uint(Bj.y));
+                  } else {
+                    const f32x2 EQ = fmul2(E, Q0[h]);      // ~ R_b delta
+                    const f32x2 D = fmul2(EQ, Q0[h]);      // delta
+                    const f32x2 P = TERMS == 2 ? ffma2(D, bc2(-0.125f), bc2(0.5f))
+                                               : ffma2(D, ffma2(D, bc2(0.0625f), bc2(-0.125f)), bc2(0.5f));
+                    tail_n(h, ffma2(EQ, P, DR0[h]), Bj.x, __float_as_uint(Bj.y));
+                  }
                 }
               }
             };
-            if (B.w == 2.f) group(std::integral_constant<int, 2>{});
-            else group(std::integral_constant<int, 3>{});
+            using T2 = std::integral_constant<int, 2>;
+            using T3 = std::integral_constant<int, 3>;
+            if (kColMono && B.w == 6.f) group(T2{}, std::true_type{});
+            else if (B.w == 2.f) group(T2{}, std::false_type{});
+            else if (kColMono && B.w == 7.f) group(T3{}, std::true_type{});
+            else group(T3{}, std::false_type{});
             c += kGroup;
           } else {
 #pragma unroll
@@ -828,11 +936,25 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           const f32x2 d0 = leg_delta2q(T0, UX[h], UY[h], W2[h], Q0[h]);
           DR2[h] = ffma2(d0, bc2(2.f), bc2(T0b.z));   // 2 dR_b + eps
         }
-        auto stage = [&](auto nrx_tag, auto terms_tag) {   // NRX > 0: the RX count at compile time
+        auto stage = [&](auto nrx_tag, auto terms_tag, auto col_tag) {   // NRX > 0: the RX count at compile time
           constexpr int NRX = decltype(nrx_tag)::value;
           constexpr int TERMS = decltype(terms_tag)::value;
+          constexpr bool COL = decltype(col_tag)::value;   // collinear stage: E = c + s (e.u), e = srec[1].xy
+          f32x2 UE[PB / 2];
+          if (COL) {
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) UE[h] = ffma2(bc2(T0b.x), UX[h], fmul2(bc2(T0b.y), UY[h]));
+          }
+          constexpr bool HORN = kHorner && TERMS <= kHornerMax;
+          f32x2 H[PB / 2][TERMS];
+          if (HORN) {
+#pragma unroll
+            for (int h = 0; h < PB / 2; ++h) horner_coef<TERMS>(Q0[h], H[h]);
+          }
           auto xleg = [&](const float4 R, const int h, const f32x2 base) {   // base + (E Q) P(delta), leg of record R
-            const f32x2 E = ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
+            const f32x2 E = COL ? ffma2(bc2(R.x), UE[h], bc2(R.z))
+                                : ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
+            if (HORN) return horner_leg<TERMS>(E, H[h], base);
             const f32x2 EQ = fmul2(E, Q0[h]);
             const f32x2 D = fmul2(EQ, Q0[h]);
             const f32x2 P = TERMS == 3
@@ -869,13 +991,16 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             }
           }
         };
-        if (SAR_BP_NRX_SPEC && a.n_rx == 4) {
-          if (T0b.w == 3.f) stage(std::integral_constant<int, 4>{}, std::integral_constant<int, 3>{});
-          else stage(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
-        } else {
-          if (T0b.w == 3.f) stage(std::integral_constant<int, 0>{}, std::integral_constant<int, 3>{});
-          else stage(std::integral_constant<int, 0>{}, std::integral_constant<int, 4>{});
-        }
+        auto dispatch = [&](auto nrx_tag) {   // srec[1].w = terms (+ 16: collinear)
+          using T3 = std::integral_constant<int, 3>;
+          using T4 = std::integral_constant<int, 4>;
+          if (T0b.w == 19.f) stage(nrx_tag, T3{}, std::true_type{});
+          else if (T0b.w == 3.f) stage(nrx_tag, T3{}, std::false_type{});
+          else if (T0b.w == 20.f) stage(nrx_tag, T4{}, std::true_type{});
+          else stage(nrx_tag, T4{}, std::false_type{});
+        };
+        if (SAR_BP_NRX_SPEC && a.n_rx == 4) dispatch(std::integral_constant<int, SAR_BP_NRX_SPEC ? 4 : 0>{});
+        else dispatch(std::integral_constant<int, 0>{});
       } else {
 #pragma unroll 1
         for (int c = 0; c < cnt; ++c) {
