@@ -605,11 +605,14 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             double ox, oy, oz;
             leg_o(k, ox, oy, oz);
             const double cj = -2.0 * (Dbx * ox + Dby * oy + Dbz * oz) + (ox * ox + oy * oy + oz * oz);
-            const float4 rec_o = col ? make_float4((float)(-2.0 * (ox * ex + oy * ey)), 0.f, (float)cj, 0.f)
+            // collinear records are {s, c, nM, window address}: one LDS.128 per RX leg
+            const float nM = (float)(nb - skw[k < items ? k : 0].x - wh + (double)kMagic);
+            const float4 rec_o = col ? make_float4((float)(-2.0 * (ox * ex + oy * ey)), (float)cj, nM,
+                                                   k < items ? srec[2 * (a.CB + k) + 1].y : 0.f)
                                      : make_float4((float)(-2.0 * ox), (float)(-2.0 * oy), (float)cj, 0.f);
             if (k < items) {
               srec[2 * (a.CB + k)] = rec_o;
-              srec[2 * (a.CB + k) + 1].x = (float)(nb - skw[k].x - wh + (double)kMagic);
+              srec[2 * (a.CB + k) + 1].x = nM;
             } else {
               srec[2 * (k - items)] = rec_o;
             }
@@ -952,7 +955,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             for (int h = 0; h < PB / 2; ++h) horner_coef<TERMS>(Q0[h], H[h]);
           }
           auto xleg = [&](const float4 R, const int h, const f32x2 base) {   // base + (E Q) P(delta), leg of record R
-            const f32x2 E = COL ? ffma2(bc2(R.x), UE[h], bc2(R.z))
+            const f32x2 E = COL ? ffma2(bc2(R.x), UE[h], bc2(R.y))
                                 : ffma2(bc2(R.x), UX[h], ffma2(bc2(R.y), UY[h], bc2(R.z)));
             if (HORN) return horner_leg<TERMS>(E, H[h], base);
             const f32x2 EQ = fmul2(E, Q0[h]);
@@ -977,14 +980,16 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
             if constexpr (NRX > 0) {
 #pragma unroll
               for (int n = 0; n < NRX; ++n, rp += 2) {
-                const float4 A = rp[0], B = rp[1];
+                const float4 A = rp[0];
+                const float2 B = COL ? make_float2(A.z, A.w) : *reinterpret_cast<const float2*>(rp + 1);
 #pragma unroll
                 for (int h = 0; h < PB / 2; ++h) tail_n(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
               }
             } else {
 #pragma unroll kRxUnroll
               for (int n = 0; n < a.n_rx; ++n, rp += 2) {
-                const float4 A = rp[0], B = rp[1];
+                const float4 A = rp[0];
+                const float2 B = COL ? make_float2(A.z, A.w) : *reinterpret_cast<const float2*>(rp + 1);
 #pragma unroll
                 for (int h = 0; h < PB / 2; ++h) tail_n(h, xleg(A, h, TS[h]), B.x, __float_as_uint(B.y));
               }
