@@ -1248,7 +1248,10 @@ template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
 #ifndef SAR_BP_BI_MINB
 #define SAR_BP_BI_MINB 4
 #endif
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? SAR_BP_BI_MINB : 1) bp_kernel_bi(const BpArgs a) {
+#ifndef SAR_BP_BI_MINB_SMALL
+#define SAR_BP_BI_MINB_SMALL 1   // other shapes (4 x 4: polar plans with wide windows)
+#endif
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW * PB == 32 ? SAR_BP_BI_MINB : NCW * PB == 16 ? SAR_BP_BI_MINB_SMALL : 1) bp_kernel_bi(const BpArgs a) {
   bp_body<true, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool BI, bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>

@@ -14,8 +14,14 @@ minf = float(sys.argv[2]) if len(sys.argv) > 2 else 0.005
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
-start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
-rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+# a multi-kernel report prints one table per kernel: keep the largest (the hot kernel's)
+starts = [i for i, l in enumerate(lines) if l.startswith('"Address"')] + [len(lines)]
+tables = []
+for s0, s1 in zip(starts, starts[1:]):
+    rs = [r for r in csv.DictReader(io.StringIO("\n".join(lines[s0:s1])))
+          if (r.get("Instructions Executed") or "0").replace(",", "").isdigit()]
+    tables.append(rs)
+rows = max(tables, key=lambda rs: sum(int(r["Instructions Executed"] or 0) for r in rs))
 tot = sum(int(r["Instructions Executed"] or 0) for r in rows)
 print(f"total warp instructions {tot:.4e}")
 blocks, cur = [], None
