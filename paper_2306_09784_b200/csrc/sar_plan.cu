@@ -248,11 +248,18 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   auto smem = [&](int cb_, int st) {
     return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic);
   };
-  if (auto_cb) {
-    cb = std::max(1, 32 / r->n_rx);
+  if (auto_cb && !bistatic) {
+    cb = 32;
     // wide windows: fewer chirps per stage so that a 2-stage ring fits in the ~56 KB that four
     // resident CTAs per SM can each have (C0, W = 59: 3 -> 4 CTAs per SM, 12.9 -> 11.7 ms)
     while (cb > 1 && smem(cb, 2) > 56 * 1024) cb /= 2;
+  } else if (auto_cb) {
+    // bistatic: long stages (~96 (chirp, RX) items) amortise the stage's base leg and records over
+    // more legs; the largest count whose 2-stage ring fits in 64 KB (3-4 resident CTAs per SM).
+    // Measured (tools/gpu_r3j.sh): C4 rank shard cb 8 -> 24: 121.0 -> 118.8 ms; C6 (W = 59) cb 2 ->
+    // 4: 11.36 -> 10.41 ms (3 CTAs per SM instead of 4), cb 6 / 8: 11.45 / 16.9 ms
+    cb = std::max(1, 96 / r->n_rx);
+    while (cb > 1 && smem(cb, 2) > 64 * 1024) --cb;
   }
   for (;;) {
     const size_t stage_bytes = smem(cb, 2) - smem(cb, 1);
