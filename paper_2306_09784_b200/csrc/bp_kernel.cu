@@ -39,4 +39,12 @@ extern "C" int sar_debug_violations_plain(unsigned long long* out4, int reset) {
   }
   return (int)e;
 }
+extern "C" int sar_debug_modes_plain(unsigned long long* out8, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, sar::g_modes, sizeof(sar::g_modes));
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(sar::g_modes, z, sizeof(z));
+  }
+  return (int)e;
+}
 #endif

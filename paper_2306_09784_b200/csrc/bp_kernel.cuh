@@ -218,8 +218,14 @@ __device__ __forceinline__ void tr_ids(int trc, int w) {
 __device__ unsigned long long g_violations[4];
 #define SAR_CHECK(cond, k) \
   if (!(cond)) atomicAdd(&g_violations[k], 1ull)
+// derived-leg modes built by the producers (tests: every mode exercised): [0] mono 2-term group,
+// [1] mono 3-term, [2] / [3] mono collinear 2 / 3 terms, [4] bistatic 3-term stage, [5] 4-term,
+// [6] / [7] bistatic collinear 3 / 4 terms
+__device__ unsigned long long g_modes[8];
+#define SAR_MODE(k) atomicAdd(&g_modes[k], 1ull)
 #else
 #define SAR_CHECK(cond, k)
+#define SAR_MODE(k)
 #endif
 
 __device__ __forceinline__ unsigned ctaid_x() {   // opaque to CSE: not kept live across loops
@@ -619,6 +625,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
               srec[2 * (k - items)] = rec_o;
             }
           }
+          if (lane == 0) SAR_MODE(4 + (tneed - 3) + (col ? 2 : 0));
           if (lane == 0)   // chirp 0's TX record: {e, eps, terms (+ 16: collinear)}
             srec[1] = make_float4((float)ex, (float)ey, (float)((kb - nb) / (double)a.A1f), (float)(tneed + (col ? 16 : 0)));
         }
@@ -672,6 +679,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
           if (c < cnt && tg <= 3) {
             const double kb = a.a1 * 2.0 * rb - a.k_lo - 0.5, nb = floor(kb);
             srec[2 * c + 1].x = (float)(nb - skw[c].x - wh + (double)kMagic);
+            if (c == cb) SAR_MODE((tg - 2) + (col ? 2 : 0));
             if (c == cb) {   // base record: the group is derived with tg terms (+ 4: collinear)
               srec[2 * c + 1].z = (float)((kb - nb) / (double)a.A1f);
               srec[2 * c + 1].w = (float)(tg + (col ? 4 : 0));
