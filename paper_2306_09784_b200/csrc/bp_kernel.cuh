@@ -475,7 +475,10 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   // derived-chirp groups: far-field monostatic tiles of plans that allow them
   // (derived stages only in the default 8 x 4 bistatic shape: in the 4 x 4 polar shape the extra
   //  code alone costs registers and measured 20 % on C6p, whose short stages gain nothing)
-  constexpr bool kDerBi = kDeriveBi && NCW == 8 && PB == 4;
+#ifndef SAR_BP_DERBI_44
+#define SAR_BP_DERBI_44 0
+#endif
+  constexpr bool kDerBi = kDeriveBi && ((NCW == 8 && PB == 4) || (SAR_BP_DERBI_44 && NCW == 4 && PB == 4));
   const bool derive = kDeriveMono && !BISTATIC && a.derive && !tile_near;
   const bool derive_bi = kDerBi && BISTATIC && a.derive && !tile_near;
 
