@@ -217,7 +217,7 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -255,7 +255,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2306_09784_b200 import sar
-    from paper_2306_09784_b200.dist import gather_rows, tile_partition, tile_row_partition
+    from paper_2306_09784_b200.dist import gather_rows, row_partition, tile_partition, tile_row_partition
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -366,6 +366,48 @@ def run_ours(args):
                 "rc_ms": [float(x) for x in allr[:, 2]], "collective_ms": [float(x) for x in allr[:, 3]],
                 "launches": plan.launches - l0, "clocks": clk.summary(), "bp_mine_ms": sum(bp_ms) / len(bp_ms)}
 
+    # ---------------- measured load balance (N > 1, outside the timed regions): tile costs depend on
+    # the geometry (near-field tiles, derived-leg series terms), so equal tile counts are not equal
+    # work.  Each rank times its BP block in a warm-up step, the blocks are re-cut on the measured
+    # cost (dist.rebalance), twice; both legs, each on its own block kind.
+    balance = {}
+    if world > 1 and not args.equal_blocks:
+        from paper_2306_09784_b200.dist import rebalance
+
+        def measured(step):
+            step()
+            step()
+            ev[2].synchronize()
+            t = torch.tensor([ev[1].elapsed_time(ev[2])], dtype=torch.float64, device=dev)
+            allt = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            return [float(x) for x in allt]
+
+        if fused is not None:
+            tblocks = [tile_partition(tiles_x * tiles_y, world, r) for r in range(world)]
+            hist = []
+            for _ in range(2):
+                times = measured(step_fused)
+                hist.append(times)
+                tblocks = [rebalance(tblocks, times, world, r) for r in range(world)]
+                t0, nt = tblocks[rank]
+            balance["fused"] = {"bp_ms_per_rank_before": hist[0], "bp_ms_per_rank_iter1": hist[1],
+                                "tiles_per_rank": [n for _, n in tblocks]}
+        rblocks = [row_partition(tiles_y, world, r) for r in range(world)]   # = tile_row_partition's blocks
+        hist = []
+        for _ in range(2):
+            times = measured(step_nccl)
+            hist.append(times)
+            rblocks = [rebalance(rblocks, times, world, r) for r in range(world)]
+            parts = [(min(g.ny, a * ty), min(g.ny, (a + n) * ty) - min(g.ny, a * ty)) for a, n in rblocks]
+            row0, nrow = parts[rank]
+            per = max(n for _, n in parts)
+            local_buf = plan.empty_image(per)
+            local_img = local_buf[:nrow]
+            full_img = torch.empty((per * world, g.nx), dtype=torch.complex64, device=dev)
+        balance["nccl"] = {"bp_ms_per_rank_before": hist[0], "bp_ms_per_rank_iter1": hist[1],
+                           "tile_rows_per_rank": [n for _, n in rblocks]}
+
     legs, check = {}, {}
     if fused is not None:
         legs["fused"] = timed(step_fused)
@@ -393,12 +435,13 @@ def run_ours(args):
     else:
         check["nccl"] = {"ok": True}
     gather = gather_summary(world, legs, check) if dist_on else None
+    if gather is not None and balance:
+        gather["balance"] = balance
     head = "nccl" if not dist_on else gather["headline"]
     if head is None:   # no leg produced the 1-GPU image: report the failure, no number
         if rank == 0:
-            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "invalid":
-                              "no gather leg reproduced the 1-GPU image", "gather": gather,
-                              "config": config_dict(args, scn)}), flush=True)
+            emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "invalid":
+                  "no gather leg reproduced the 1-GPU image", "gather": gather, "config": config_dict(args, scn)})
         plan.close()
         if dist_on:
             dist.destroy_process_group()
@@ -520,7 +563,7 @@ def run_ours(args):
             "gpu_launches": leg["launches"],
             "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     plan.close()
     if dist_on:
         dist.destroy_process_group()
@@ -637,7 +680,7 @@ def run_stream(args):
                     "30 m x 12 m grid at 1 cm re-centred per frame")
         step = "one frame: sar_range_compress + sar_backproject of this rank's chirps (+ reduce)"
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": STREAM_METRIC,
             "value": upd / (ms_frame * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_frame, "max_frame_ms": float(tot[1]),
@@ -650,12 +693,31 @@ def run_stream(args):
                            else " + NCCL reduce"),
                        "step": step},
             "gpu_launches": launches, "clocks": clk.summary(),
-        }), flush=True)
+        })
     for p in plans:
         p.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+_OUT = None   # the process's real stdout once main() has claimed it (see _claim_stdout)
+
+
+def _claim_stdout():
+    """The JSON line is the only stdout line: keep the real stdout on a private descriptor and point
+    descriptor 1 at stderr, so that anything else a library prints there (NCCL's version banner, which
+    rank 0 of a process group prints on stdout whatever NCCL_DEBUG says) cannot precede or split it."""
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w", buffering=1)
+        os.dup2(2, 1)
+    return _OUT
+
+
+def emit(obj):
+    print(json.dumps(obj), file=_OUT or sys.stdout, flush=True)
 
 
 def main(argv=None):
@@ -671,6 +733,8 @@ def main(argv=None):
     ap.add_argument("--cpu-s", type=float, default=12.0, help="seconds of oracle BP for cpu_baseline")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds of oracle BP per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--equal-blocks", action="store_true",
+                    help="N > 1: equal tile (row) counts per rank, no measured load balance")
     ap.add_argument("--all-legs", action="store_true",
                     help="N = 1 check run: a one-rank process group, both gather legs timed and checked")
     ap.add_argument("--gather", default="auto", choices=["auto", "fused", "multicast", "nccl"],
@@ -679,6 +743,7 @@ def main(argv=None):
                          "NVSwitch multicast address; symmetric memory); nccl: the NCCL leg only.  C5: the "
                          "chirp-shard reduction is an NCCL reduce unless fused/multicast (P2P red.add)")
     args = ap.parse_args(argv)
+    _claim_stdout()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
@@ -708,10 +773,10 @@ def self_launch(args, argv):
         ngpu = 0
     if ngpu < args.gpus:
         legs = {"fused": None, "nccl": None}
-        print(json.dumps({"metric": METRIC if args.config not in ("C5", "C5i") else STREAM_METRIC, "value": None,
-                          "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                          "unavailable": f"--gpus {args.gpus}: {ngpu} GPU(s) visible",
-                          "gather": gather_summary(args.gpus, legs, {})}), flush=True)
+        emit({"metric": METRIC if args.config not in ("C5", "C5i") else STREAM_METRIC, "value": None,
+              "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+              "unavailable": f"--gpus {args.gpus}: {ngpu} GPU(s) visible",
+              "gather": gather_summary(args.gpus, legs, {})})
         return 0
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -720,7 +785,8 @@ def self_launch(args, argv):
     argv = list(sys.argv[1:] if argv is None else argv)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
-    return subprocess.call(cmd)
+    # the ranks write their JSON line to this process's real stdout (descriptor 1 points at stderr)
+    return subprocess.call(cmd, stdout=_OUT)
 
 
 if __name__ == "__main__":

@@ -40,6 +40,41 @@ def tile_row_partition(tiles_y: int, tile_y: int, ny: int, world: int, rank: int
     return row0, min(ny, (t0 + nt) * tile_y) - row0
 
 
+def weighted_partition(weights, world: int, rank: int):
+    """Contiguous blocks of items with about equal total weight, as (first, count): block r ends
+    at the item boundary nearest to (r + 1)/world of the total, every block keeps at least one item
+    when there are at least ``world`` items.  With equal weights it is ``row_partition``'s split."""
+    import bisect
+
+    n = len(weights)
+    cum = [0.0]
+    for w in weights:
+        cum.append(cum[-1] + max(float(w), 0.0))
+    if cum[-1] <= 0.0 or n < world:
+        return row_partition(n, world, rank)
+    cuts = [0]
+    for k in range(1, world):
+        target = cum[-1] * k / world
+        i = bisect.bisect_left(cum, target)
+        if i > n or (i > 0 and target - cum[i - 1] <= cum[i] - target):
+            i -= 1
+        cuts.append(min(max(i, cuts[-1] + 1), n - (world - k)))
+    cuts.append(n)
+    return cuts[rank], cuts[rank + 1] - cuts[rank]
+
+
+def rebalance(blocks, times, world: int, rank: int):
+    """Measured load balance: re-cut contiguous blocks (``blocks`` = every rank's (first, count) over
+    the same item sequence, ``times`` = every rank's measured time for its block) so that each rank
+    gets an equal share of the measured cost, the cost spread uniformly over each measured block.
+    Used by ``bench.py`` between warm-up steps (tile costs depend on the geometry: near-field tiles,
+    derived-leg series terms), converging in a couple of iterations."""
+    w = []
+    for (_, n), t in sorted(zip(blocks, times)):
+        w += [max(float(t), 0.0) / n] * n if n > 0 else []
+    return weighted_partition(w, world, rank)
+
+
 def chirp_partition(n_chirps: int, world: int, rank: int):
     return row_partition(n_chirps, world, rank)
 

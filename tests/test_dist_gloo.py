@@ -13,8 +13,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import sarsim
-from paper_2306_09784_b200.dist import (chirp_partition, gather_rows, reduce_partials, row_partition, tile_partition,
-                                       tile_row_partition)
+from paper_2306_09784_b200.dist import (chirp_partition, gather_rows, rebalance, reduce_partials, row_partition,
+                                       tile_partition, tile_row_partition, weighted_partition)
 
 
 def _free_port():
@@ -108,3 +108,27 @@ def test_tile_partitions_cover_exactly():
                 assert a + na == b and (na == 0 or a % ty == 0)
             full = [n for _, n in parts if n > 0][:-1]
             assert all(n % ty == 0 for n in full)
+
+
+def test_weighted_partition_and_measured_rebalance():
+    """Cost-balanced contiguous blocks (bench.py's measured load balance): they cover the items
+    exactly, equal weights give blocks balanced to +-1 item, and re-cutting equal blocks on measured
+    block times whose cost per item falls with the index (C3: tile rows near the track cost more)
+    brings the predicted per-rank costs within one item's cost of each other."""
+    for n in (8, 94, 8836):
+        for w in (1, 2, 3, 8):
+            blocks = [weighted_partition([1.0] * n, w, r) for r in range(w)]
+            assert blocks[0][0] == 0 and sum(b for _, b in blocks) == n
+            for (a, na), (b, _) in zip(blocks, blocks[1:]):
+                assert a + na == b
+            assert max(b for _, b in blocks) - min(b for _, b in blocks) <= 1
+    cost = [1.0 + 0.1 * (1.0 - i / 8835) for i in range(8836)]   # true per-tile cost
+    for w in (2, 4, 8):
+        blocks = [tile_partition(8836, w, r) for r in range(w)]
+        for _ in range(3):
+            times = [sum(cost[a:a + n]) for a, n in blocks]
+            blocks = [rebalance(blocks, times, w, r) for r in range(w)]
+            assert blocks[0][0] == 0 and sum(n for _, n in blocks) == 8836
+        times = [sum(cost[a:a + n]) for a, n in blocks]
+        assert max(times) - min(times) <= 2 * max(cost)
+    assert weighted_partition([0.0] * 5, 2, 0) == row_partition(5, 2, 0)   # no measured cost: equal blocks

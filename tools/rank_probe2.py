@@ -11,7 +11,7 @@ import torch
 
 import sarsim
 from paper_2306_09784_b200 import sar
-from paper_2306_09784_b200.dist import tile_partition, tile_row_partition
+from paper_2306_09784_b200.dist import rebalance, row_partition, tile_partition
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 worlds = [int(w) for w in sys.argv[2:]] or [2, 4, 8]
@@ -45,15 +45,23 @@ print(f"{cfg} 1-GPU backproject {t1:.3f} ms")
 for world in worlds:
     imgs = [torch.zeros((g.ny, g.nx), dtype=torch.complex64, device=dev) for _ in range(min(world, 8))]
     ptrs = [im.data_ptr() for im in imgs]
-    fused, rows = [], []
-    for r in range(world):
-        t0, nt = tile_partition(tiles_x * tiles_y, world, r)
-        fused.append(timed(lambda: plan.backproject_scatter_tiles(prof, tx, ptrs, t0, nt, rx)))
-        row0, nrow = tile_row_partition(tiles_y, plan.info.tile_y, g.ny, world, r)
-        out = torch.empty((max(nrow, 1), g.nx), dtype=torch.complex64, device=dev)
-        rows.append(timed(lambda: plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=out[:nrow])))
     ideal = t1 / world
-    print(f"N={world}: fused per rank {['%.3f' % t for t in fused]} max {max(fused):.3f} ({max(fused) / ideal:.3f} x ideal)")
-    print(f"N={world}: tile rows per rank {['%.3f' % t for t in rows]} max {max(rows):.3f} ({max(rows) / ideal:.3f} x ideal)")
+    # bench.py's measured load balance: equal blocks, then two re-cuts on the measured block times
+    tb = [tile_partition(tiles_x * tiles_y, world, r) for r in range(world)]
+    rb = [row_partition(tiles_y, world, r) for r in range(world)]
+    ty = plan.info.tile_y
+    for it in range(3):
+        fused = [timed(lambda: plan.backproject_scatter_tiles(prof, tx, ptrs, t0, nt, rx)) for t0, nt in tb]
+        rows = []
+        for a, n in rb:
+            row0, nrow = min(g.ny, a * ty), min(g.ny, (a + n) * ty) - min(g.ny, a * ty)
+            out = torch.empty((max(nrow, 1), g.nx), dtype=torch.complex64, device=dev)
+            rows.append(timed(lambda: plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=out[:nrow])))
+        label = "equal blocks" if it == 0 else f"rebalanced x{it}"
+        for name, ts in (("fused (tile blocks)", fused), ("NCCL leg (tile rows)", rows)):
+            print(f"N={world} {label}: {name} per rank {['%.3f' % t for t in ts]} max {max(ts):.3f} "
+                  f"({max(ts) / ideal:.3f} x ideal, spread {(max(ts) - min(ts)) / max(ts):.1%})")
+        tb = [rebalance(tb, fused, world, r) for r in range(world)]
+        rb = [rebalance(rb, rows, world, r) for r in range(world)]
     del imgs
 plan.close()
