@@ -371,7 +371,7 @@ def run_ours(args):
     # work.  Each rank times its BP block in a warm-up step, the blocks are re-cut on the measured
     # cost (dist.rebalance), twice; both legs, each on its own block kind.
     balance = {}
-    if world > 1 and not args.equal_blocks:
+    if dist_on and not args.equal_blocks:   # (a one-rank --all-legs run exercises the same path)
         from paper_2306_09784_b200.dist import rebalance
 
         def measured(step):
