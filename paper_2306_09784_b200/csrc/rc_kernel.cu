@@ -222,11 +222,24 @@ struct RcWarpPlan {
 };
 
 // One radix-R Stockham stage over a warp's row (NS = product of the radices before it):
-// butterfly j takes in[j + r L/R], twiddles by W_(NS R)^((j mod NS) r) (table stw[k][R]),
-// and writes its natural-order outputs to (j / NS) NS R + (j mod NS) + r NS.  Lane addresses
-// are one base per butterfly plus compile-time offsets (rpos(i + 8 m) = rpos(i) + 9 m).
+// butterfly j takes in[j + r L/R], twiddles by W_(NS R)^((j mod NS) r), and writes its
+// natural-order outputs to (j / NS) NS R + (j mod NS) + r NS.  Lane addresses are one base per
+// butterfly plus compile-time offsets (rpos(i + 8 m) = rpos(i) + 9 m).  The twiddles are the
+// powers w^r of the butterfly's base w = W_(NS R)^(j mod NS) (fp64-built, held in registers for
+// the whole kernel), formed with at most three chained multiplications: loading R - 1 twiddles
+// per butterfly from the plan table cost 23 % of the kernel's time (L1 wavefronts).
+template <int R>
+__device__ __forceinline__ void twiddle_powers(float2* v, const float2 w1) {
+  float2 w[R];
+  w[1] = w1;
+#pragma unroll
+  for (int r = 2; r < R; ++r) w[r] = (r % 2 == 0) ? cmul(w[r / 2], w[r / 2]) : cmul(w[r - 1], w1);
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+}
+
 template <int L, int R, int NS>
-__device__ __forceinline__ void stockham_stage(float2* v, float2* row, const float2* __restrict__ stw, int lane) {
+__device__ __forceinline__ void stockham_stage(float2* v, float2* row, const float2* base, int lane) {
   constexpr int B = L / (32 * R);                  // butterflies per lane
   static_assert((L / R) % 8 == 0 && NS % 8 == 0, "stage offsets must be multiples of 8");
 #pragma unroll
@@ -238,15 +251,7 @@ __device__ __forceinline__ void stockham_stage(float2* v, float2* row, const flo
   __syncwarp();
 #pragma unroll
   for (int s = 0; s < B; ++s) {
-    const int j = lane + 32 * s;
-    const int k = j % NS;
-    const float4* w4 = reinterpret_cast<const float4*>(stw + k * R);
-#pragma unroll
-    for (int h = 0; h < R / 2; ++h) {
-      const float4 w = __ldg(w4 + h);
-      if (h) v[s * R + 2 * h] = cmul(v[s * R + 2 * h], make_float2(w.x, w.y));
-      v[s * R + 2 * h + 1] = cmul(v[s * R + 2 * h + 1], make_float2(w.z, w.w));
-    }
+    twiddle_powers<R>(v + s * R, base[s]);
     dft<R>(v + s * R);
   }
 #pragma unroll
@@ -292,6 +297,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
     __syncthreads();
   }
 
+  // twiddle bases of this lane's butterflies: stage 1 W_64^(j mod 8), stage 2 W_L^(j mod 64)
+  constexpr int R2 = L / 64, B1 = L / (32 * 8), B2 = L / (32 * R2);
+  float2 tw1[B1], tw2[B2];
+#pragma unroll
+  for (int s = 0; s < B1; ++s) tw1[s] = __ldg(a.stw + ((lane + 32 * s) % 8) * 8 + 1);
+#pragma unroll
+  for (int s = 0; s < B2; ++s) tw2[s] = __ldg(a.stw + 64 + ((lane + 32 * s) % 64) * R2 + 1);
+
   int it = 0;
   for (int pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
     const int ra = a.row0 + 2 * pair;
@@ -333,8 +346,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
         for (int r = 0; r < 8; ++r) dst[r] = v[r];
       }
       __syncwarp();
-      stockham_stage<L, 8, 8>(v, row, a.stw, lane);
-      stockham_stage<L, L / 64, 64>(v, row, a.stw + 64, lane);
+      stockham_stage<L, 8, 8>(v, row, tw1, lane);
+      stockham_stage<L, L / 64, 64>(v, row, tw2, lane);
     }
     __syncthreads();   // spectrum complete; the raw slot is consumed
     if (RING > 0 && threadIdx.x == 0 && pair + RING * (int)gridDim.x < npairs)
@@ -356,7 +369,16 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
     const float2* zn = xs + (hn & (zp - 1)) * RS + rpos(hn >> lzp);
     const int dstep = rpos(kStep >> lzp);   // row positions per block step (kStep / zp is a multiple of 8)
     const bool lin = (kStep % zp) == 0 && ((kStep >> lzp) & 7) == 0 && a.k_lo > 0;
-    for (int i = threadIdx.x; i < a.n_bins; i += kStep, zk += dstep, zn -= dstep) {
+    // centring ramp exp(+j 2 pi k t_c / N): the table entry of the thread's first bin, then one
+    // multiplication by the block step's ramp exp(+j 2 pi kStep t_c / N) per step (read from the
+    // table as ramp[kStep] conj(ramp[0])): one load per thread instead of one per bin
+    float2 rr = __ldg(a.ramp + min((int)threadIdx.x, a.n_bins - 1));
+    float2 rstep = make_float2(1.f, 0.f);
+    if (a.n_bins > kStep) {
+      const float2 r0 = __ldg(a.ramp), rk = __ldg(a.ramp + kStep);
+      rstep = make_float2(rk.x * r0.x + rk.y * r0.y, rk.y * r0.x - rk.x * r0.y);
+    }
+    for (int i = threadIdx.x; i < a.n_bins; i += kStep, zk += dstep, zn -= dstep, rr = cmul(rr, rstep)) {
       const int k = a.k_lo + i;
       float2 Zk, Zn;
       if (lin) {
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
         Zk = xs[(k & (zp - 1)) * RS + rpos(k >> lzp)];
         Zn = xs[(kn & (zp - 1)) * RS + rpos(kn >> lzp)];
       }
-      const float2 r = __ldg(a.ramp + i);
+      const float2 r = rr;
       const float2 A = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
       const float2 B = make_float2(0.5f * (Zk.y + Zn.y), -0.5f * (Zk.x - Zn.x));
       const float2 Ar = cmul(A, r), Br = cmul(B, r);
