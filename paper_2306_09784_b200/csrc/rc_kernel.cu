@@ -311,8 +311,9 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
     const bool has_b = 2 * pair + 1 < a.nrows;
     const float* xa;
     if (RING > 0) {
-      const int slot = it % RING;
-      mbar_wait(bar0 + 8 * slot, (uint32_t)(it / RING) & 1u);
+      constexpr int kR = RING > 0 ? RING : 1;   // (RING = 0 instantiations never take this branch)
+      const int slot = it % kR;
+      mbar_wait(bar0 + 8 * slot, (uint32_t)(it / kR) & 1u);
       xa = ring + slot * 2 * a.ns;
     } else {
       xa = a.raw + (size_t)ra * a.ns;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 8 ? SAR_RC_MINB : 1) rc_k
     }
     __syncthreads();   // spectrum complete; the raw slot is consumed
     if (RING > 0 && threadIdx.x == 0 && pair + RING * (int)gridDim.x < npairs)
-      issue(pair + RING * gridDim.x, it % RING);
+      issue(pair + RING * gridDim.x, it % (RING > 0 ? RING : 1));
 
     // epilogue as in rc_kernel, Z[k] = Xs[k mod zp][k / zp]
     const int ma = ra / a.n_rx, mb = (ra + 1) / a.n_rx;
