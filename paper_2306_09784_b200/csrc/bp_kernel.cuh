@@ -1241,20 +1241,25 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   }
 }
 
-// Register budget: the monostatic kernel is left to ptxas (a min-blocks bound changes its
-// schedule and was measured 5 % slower on C3); the bistatic kernel (TX leg kept live across
-// the RX loop) is held to four resident CTAs per SM at the default 32 x 32 tile:
+// Register budget: the monostatic kernel is held to three resident CTAs per SM (below), the
+// bistatic kernel (TX leg kept live across the RX loop) to four at the default 32 x 32 tile:
 // C4 1343 -> 1190 ms (tools/vsweep.sh).
 #ifndef SAR_BP_MONO_MINB
-#define SAR_BP_MONO_MINB 4
+// three resident CTAs per SM (72 registers): with the integer-index tails and 2-term Horner groups
+// the fourth CTA no longer pays for the spills of the 56-register floor (C3 51.76 -> 50.73 ms, C0
+// 9.20 -> 8.90, C2 21.43 -> 20.77; in round 1 and early round 2 the floor of four measured faster)
+#define SAR_BP_MONO_MINB 3
 #endif
 // resident-CTA floor per shape (register cap ~56-113): ptxas otherwise spends registers on ILP of
 // the unrolled derived groups (4 x 4: 64 -> 120 registers) and the occupancy collapses
-constexpr int mono_min_blocks(int ncw, int pb) {
-  return ncw == 8 && pb == 4 ? SAR_BP_MONO_MINB : ncw == 4 && pb == 4 ? 6 : ncw == 4 && pb == 8 ? 4 : 2;
+#ifndef SAR_BP_SCATTER_MINB
+#define SAR_BP_SCATTER_MINB SAR_BP_MONO_MINB
+#endif
+constexpr int mono_min_blocks(int ncw, int pb, bool scatter) {
+  return ncw == 8 && pb == 4 ? (scatter ? SAR_BP_SCATTER_MINB : SAR_BP_MONO_MINB) : ncw == 4 && pb == 4 ? 6 : ncw == 4 && pb == 8 ? 4 : 2;
 }
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
-__global__ void __launch_bounds__((NCW + 1) * 32, mono_min_blocks(NCW, PB)) bp_kernel_mono(const BpArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, mono_min_blocks(NCW, PB, SCATTER)) bp_kernel_mono(const BpArgs a) {
   bp_body<false, DOP, NEAR, NCW, PB, SCATTER>(a);
 }
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>

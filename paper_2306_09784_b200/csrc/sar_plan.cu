@@ -248,12 +248,14 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   auto smem = [&](int cb_, int st) {
     return sar::bp_smem_bytes(I.window_bins, cb_, r->n_rx, st, bistatic);
   };
+  // ring budget per CTA: the monostatic kernel keeps three CTAs per SM resident (72 registers),
+  // so up to ~64 KB each; wide windows take fewer chirps per stage (in steps of the derived-chirp
+  // group while possible).  Measured (tools/gpu_r4e.sh): C0 (W = 59) 32 chirps x 2 stages 8.85 ms vs
+  // 24: 8.93, 16: 9.16; C3 (W = 26) 4 stages of 32: 50.31 ms vs 3: 50.73, 2: 51.42
+  const size_t ring_budget = bistatic ? 48 * 1024 : 64 * 1024;
   if (auto_cb && !bistatic) {
     cb = 32;
-    // wide windows: fewer chirps per stage so that a 2-stage ring fits in the ~56 KB that four
-    // resident CTAs per SM can each have (C0, W = 59: 3 -> 4 CTAs per SM, 12.9 -> 11.7 ms), in
-    // steps of the derived-chirp group while possible (C0: 24 chirps, 9.41 -> 9.20 ms vs 16)
-    while (cb > 1 && smem(cb, 2) > 56 * 1024) cb = cb > 8 ? cb - 8 : cb / 2;
+    while (cb > 1 && smem(cb, 2) > 64 * 1024) cb = cb > 8 ? cb - 8 : cb / 2;
   } else if (auto_cb) {
     // bistatic: long stages (~96 (chirp, RX) items) amortise the stage's base leg and records over
     // more legs; the largest count whose 2-stage ring fits in 64 KB (3-4 resident CTAs per SM).
@@ -265,8 +267,8 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
   for (;;) {
     const size_t stage_bytes = smem(cb, 2) - smem(cb, 1);
     int st = stages;
-    // ring depth: as many stages as fit in ~48 KB
-    if (auto_stages) st = (int)std::min<size_t>(sar::kBpMaxStages, (48 * 1024) / std::max<size_t>(1, stage_bytes));
+    // ring depth: as many stages as fit in the budget
+    if (auto_stages) st = (int)std::min<size_t>(sar::kBpMaxStages, ring_budget / std::max<size_t>(1, stage_bytes));
     st = std::max(2, std::min(sar::kBpMaxStages, st));
     if (smem(cb, st) <= 200 * 1024) {
       stages = st;
