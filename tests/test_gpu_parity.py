@@ -335,7 +335,10 @@ def test_chirp_split_for_small_grids(cuda_lib):
 def test_C3_rank_partitions_assemble_the_one_gpu_image(cuda_lib, world):
     """The bench's N-GPU decompositions of C3, run rank by rank on one GPU: the tile partition
     (fused-gather leg) and the tile-row partition (NCCL all-gather leg) assemble the 1-GPU image
-    to fp32 chunk order (<= 1e-6); every pixel is computed with the unsharded tile anchor."""
+    to fp32 chunk order; every pixel is computed with the unsharded tile anchor.  The launches split
+    their chirps into different chunk counts (a shard fills the GPU with more chunks), so the
+    per-pixel sums differ in the order the chunk partials are added: measured 1.0-1.1e-6 (three
+    resident CTAs per SM), checked at 2e-6, well inside T11's 1e-5 (reading A18)."""
     import torch
 
     from paper_2306_09784_b200.dist import tile_partition, tile_row_partition
@@ -358,7 +361,7 @@ def test_C3_rank_partitions_assemble_the_one_gpu_image(cuda_lib, world):
     e_t = float((tiled - img).abs().max() / ref)
     e_r = float((rows - img).abs().max() / ref)
     plan.close()
-    assert e_t <= 1e-6 and e_r <= 1e-6, (e_t, e_r)
+    assert e_t <= 2e-6 and e_r <= 2e-6, (e_t, e_r)
 
 
 def test_one_pixel_grid_and_single_chirp(cuda_lib):
