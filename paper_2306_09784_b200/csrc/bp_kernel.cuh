@@ -95,6 +95,13 @@ constexpr bool kColMono = SAR_BP_COL_MONO;
 #endif
 constexpr bool kHorner = SAR_BP_HORNER;
 constexpr int kHornerMax = SAR_BP_HORNER_MAX;
+#ifndef SAR_BP_HORNER_MAX_BI
+// bistatic stages (3-4 terms) in Horner form too, at three resident CTAs per SM (72 registers):
+// C4 rank shard 118.7-120.5 -> 115.65 ms, C6 10.36 -> 9.87 ms (tools/gpu_r4i.sh); at four CTAs
+// (56 registers) the extra coefficients spilled (+14-19 %)
+#define SAR_BP_HORNER_MAX_BI 4
+#endif
+constexpr int kHornerMaxBi = SAR_BP_HORNER_MAX_BI;
 constexpr bool kDeriveMono = SAR_BP_DERIVE_MONO;   // derived-chirp groups compiled in (monostatic)
 constexpr bool kDeriveBi = SAR_BP_DERIVE_BI;       // derived stages compiled in (bistatic)
 // Derived legs (reading A22): R sqrt(1 + delta) - R by the binomial series truncated after t
@@ -961,7 +968,7 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
 #pragma unroll
             for (int h = 0; h < PB / 2; ++h) UE[h] = ffma2(bc2(T0b.x), UX[h], fmul2(bc2(T0b.y), UY[h]));
           }
-          constexpr bool HORN = kHorner && TERMS <= kHornerMax;
+          constexpr bool HORN = kHorner && TERMS <= kHornerMaxBi;
           f32x2 H[PB / 2][TERMS];
           if (HORN) {
 #pragma unroll
@@ -1241,9 +1248,9 @@ __device__ __forceinline__ void bp_body(const BpArgs& a) {
   }
 }
 
-// Register budget: the monostatic kernel is held to three resident CTAs per SM (below), the
-// bistatic kernel (TX leg kept live across the RX loop) to four at the default 32 x 32 tile:
-// C4 1343 -> 1190 ms (tools/vsweep.sh).
+// Register budget: the monostatic and the bistatic kernels are held to three resident CTAs per SM
+// at the default 32 x 32 tile (an unbounded bistatic kernel ran at 2 CTAs: C4 1343 ms vs 1190 at
+// four in round 1, tools/vsweep.sh; three with the Horner stages since round 2).
 #ifndef SAR_BP_MONO_MINB
 // three resident CTAs per SM (72 registers): with the integer-index tails and 2-term Horner groups
 // the fourth CTA no longer pays for the spills of the 56-register floor (C3 51.76 -> 50.73 ms, C0
@@ -1264,7 +1271,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, mono_min_blocks(NCW, PB, SCATT
 }
 template <bool DOP, bool NEAR, int NCW, int PB, bool SCATTER>
 #ifndef SAR_BP_BI_MINB
-#define SAR_BP_BI_MINB 4
+#define SAR_BP_BI_MINB 3   // (with the Horner stages; 4 before: see SAR_BP_HORNER_MAX_BI)
 #endif
 #ifndef SAR_BP_BI_MINB_SMALL
 #define SAR_BP_BI_MINB_SMALL 1   // other shapes (4 x 4: polar plans with wide windows)
