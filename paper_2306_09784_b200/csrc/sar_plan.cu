@@ -257,11 +257,12 @@ sar_status_t derive(const sar_radar_params_t* r, const sar_grid_t* g, const sar_
     cb = 32;
     while (cb > 1 && smem(cb, 2) > 64 * 1024) cb = cb > 8 ? cb - 8 : cb / 2;
   } else if (auto_cb) {
-    // bistatic: long stages (~96 (chirp, RX) items) amortise the stage's base leg and records over
-    // more legs; the largest count whose 2-stage ring fits in 64 KB (3-4 resident CTAs per SM).
-    // Measured (tools/gpu_r3j.sh): C4 rank shard cb 8 -> 24: 121.0 -> 118.8 ms; C6 (W = 59) cb 2 ->
-    // 4: 11.36 -> 10.41 ms (3 CTAs per SM instead of 4), cb 6 / 8: 11.45 / 16.9 ms
-    cb = std::max(1, 96 / r->n_rx);
+    // bistatic: long stages (~64 (chirp, RX) items) amortise the stage's base leg and records over
+    // more legs; the largest count whose 2-stage ring fits in 64 KB.  Measured (tools/gpu_r3j.sh,
+    // r4k.sh): C4 rank shard cb 8 -> 24: 121.0 -> 118.8 ms at four CTAs per SM; at three with Horner
+    // stages cb 16 / 20 / 24 / 32: 114.1 / 116.0 / 115.6 / 117.2 ms (shorter stages keep more of them
+    // within 3 series terms); C6 (W = 59) cb 2 -> 4: 11.36 -> 10.41 ms, cb 6 / 8: 11.45 / 16.9 ms
+    cb = std::max(1, 64 / r->n_rx);
     while (cb > 1 && smem(cb, 2) > 64 * 1024) --cb;
   }
   for (;;) {
