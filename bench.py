@@ -234,17 +234,17 @@ L2_NOTE = "256 MB buffer written between timed steps (outside the event span)"
 
 
 def gather_summary(world, legs, check):
-    """N > 1: both gather legs of the same run.  ``legs`` maps "fused" / "nccl" to
+    """N > 1: the gather legs of the same run.  ``legs`` maps "fused" / "publish" / "nccl" to
     {"ms": per-step ms (max over ranks), "bp_ms": per-rank BP ms list, "collective_ms": per-rank
     ms of the collective / barrier after the BP} or None when the leg did not run."""
     out = {"world": world, "headline": None}
-    for name in ("fused", "nccl"):
+    for name in ("fused", "publish", "nccl"):
         leg = legs.get(name)
         out[f"{name}_ms"] = None if leg is None else leg["ms"]
         out[f"{name}_bp_ms_per_rank"] = None if leg is None else leg["bp_ms"]
         out[f"{name}_collective_ms_per_rank"] = None if leg is None else leg["collective_ms"]
         out[f"{name}_check"] = check.get(name)
-    ok = [n for n in ("fused", "nccl") if legs.get(n) is not None and (check.get(n) or {}).get("ok")]
+    ok = [n for n in ("fused", "publish", "nccl") if legs.get(n) is not None and (check.get(n) or {}).get("ok")]
     if ok:
         out["headline"] = min(ok, key=lambda n: legs[n]["ms"])
     return out
@@ -288,13 +288,17 @@ def run_ours(args):
     local_img = local_buf[:nrow]
     full_img = torch.empty((per * world, g.nx), dtype=torch.complex64, device=dev) if dist_on else local_img
     fused, fused_err = None, None
-    if dist_on and args.gather in ("auto", "fused", "multicast"):
+    if dist_on and args.gather in ("auto", "fused", "publish", "multicast"):
         from paper_2306_09784_b200.dist import FusedRowGather
 
         try:
             fused = FusedRowGather(g.ny, g.nx, dev, prefer_multicast=args.gather == "multicast")
         except Exception as e:  # no symmetric memory on this system: the NCCL leg alone
             fused_err = repr(e)[:200]
+    # publish leg (SAR_SCATTER_PUBLISH): plain BP of the rank's tile block into its own symmetric
+    # image, then one copy of the finished tiles to the peers' images
+    pub_ptrs = fused.publish_ptrs(rank) if fused is not None and args.gather in ("auto", "publish") else None
+    p0, pn = t0, nt
     polar = plan.polar
     if polar:   # Measure E: the polar image is resampled onto the Cartesian C0 grid in the step
         import sarsim
@@ -309,6 +313,15 @@ def run_ours(args):
         plan.range_compress(raw, wsar, out=prof, stream=stream)
         ev[1].record(stream)
         plan.backproject_scatter_tiles(prof, tx, fused.ptrs, t0, nt, rx, multicast=fused.multicast, stream=stream)
+        ev[2].record(stream)
+        fused.barrier()
+        if polar:
+            sar.polar_to_cartesian(g, fused.image, cart, out=cart_img, stream=stream)
+
+    def step_publish():
+        plan.range_compress(raw, wsar, out=prof, stream=stream)
+        ev[1].record(stream)
+        plan.backproject_scatter_tiles(prof, tx, pub_ptrs, p0, pn, rx, publish=True, stream=stream)
         ev[2].record(stream)
         fused.barrier()
         if polar:
@@ -383,7 +396,7 @@ def run_ours(args):
             dist.all_gather(allt, t)
             return [float(x) for x in allt]
 
-        if fused is not None:
+        if fused is not None and args.gather != "publish":
             tblocks = [tile_partition(tiles_x * tiles_y, world, r) for r in range(world)]
             hist = []
             for _ in range(2):
@@ -393,6 +406,16 @@ def run_ours(args):
                 t0, nt = tblocks[rank]
             balance["fused"] = {"bp_ms_per_rank_before": hist[0], "bp_ms_per_rank_iter1": hist[1],
                                 "tiles_per_rank": [n for _, n in tblocks]}
+        if pub_ptrs is not None:
+            pblocks = [tile_partition(tiles_x * tiles_y, world, r) for r in range(world)]
+            hist = []
+            for _ in range(2):
+                times = measured(step_publish)
+                hist.append(times)
+                pblocks = [rebalance(pblocks, times, world, r) for r in range(world)]
+                p0, pn = pblocks[rank]
+            balance["publish"] = {"bp_ms_per_rank_before": hist[0], "bp_ms_per_rank_iter1": hist[1],
+                                  "tiles_per_rank": [n for _, n in pblocks]}
         rblocks = [row_partition(tiles_y, world, r) for r in range(world)]   # = tile_row_partition's blocks
         hist = []
         for _ in range(2):
@@ -408,9 +431,15 @@ def run_ours(args):
         balance["nccl"] = {"bp_ms_per_rank_before": hist[0], "bp_ms_per_rank_iter1": hist[1],
                            "tile_rows_per_rank": [n for _, n in rblocks]}
 
-    legs, check = {}, {}
-    if fused is not None:
+    legs, check, snaps = {}, {}, {}
+    if fused is not None and args.gather != "publish":
         legs["fused"] = timed(step_fused)
+        if dist_on:
+            snaps["fused"] = fused.image.clone()   # (the publish leg reuses the symmetric image)
+    if pub_ptrs is not None:
+        legs["publish"] = timed(step_publish)
+        if dist_on:
+            snaps["publish"] = fused.image.clone()
     legs["nccl"] = timed(step_nccl)
     # ---------------- outside the timed regions: every leg's image against this plan's 1-GPU image
     # (every pixel is computed in its absolute tile: equal up to the fp32 order of chirp-chunk sums)
@@ -419,9 +448,7 @@ def run_ours(args):
         ref = plan.backproject(prof, tx, rx, stream=stream)
         torch.cuda.synchronize()
         scale = ref.abs().max().clamp_min(1e-30)
-        imgs = {"nccl": image_of_nccl()}
-        if fused is not None:
-            imgs["fused"] = fused.image
+        imgs = {"nccl": image_of_nccl(), **snaps}
         for name, im in imgs.items():
             rel = float((im - ref).abs().max() / scale)
             # T11: 1e-5, the fp32 order of chirp-chunk sums (legs split their chirps
@@ -455,10 +482,11 @@ def run_ours(args):
     peaks = _peaks()
     clocks = leg["clocks"]
     max_mhz = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
-    if head == "fused":
+    if head in ("fused", "publish"):
         # pixels of the rank's tiles (ragged last tile column / row clipped to the grid)
-        ntx = [min(32, g.nx - 32 * (t % tiles_x)) for t in range(t0, t0 + nt)]
-        nty = [min(ty, g.ny - ty * (t // tiles_x)) for t in range(t0, t0 + nt)]
+        b0, bn = (t0, nt) if head == "fused" else (p0, pn)
+        ntx = [min(32, g.nx - 32 * (t % tiles_x)) for t in range(b0, b0 + bn)]
+        nty = [min(ty, g.ny - ty * (t // tiles_x)) for t in range(b0, b0 + bn)]
         bp_px = sum(a * b for a, b in zip(ntx, nty))
     else:
         bp_px = nrow * g.nx
@@ -538,6 +566,11 @@ def run_ours(args):
                    f"({'multimem.st' if fused.multicast else 'P2P stores'}, symmetric memory)")
             step_txt = ("sar_range_compress(all chirps) + sar_backproject_scatter_tiles(rank tiles -> every "
                         "rank's image) + symmetric-memory barrier")
+        elif head == "publish":
+            par = (f"pixel tiles x{world} (balanced tile blocks) + BP into the own symmetric-memory image, "
+                   f"then one copy of the finished tiles to every peer (P2P stores)")
+            step_txt = ("sar_range_compress(all chirps) + sar_backproject_scatter_tiles(SAR_SCATTER_PUBLISH: rank "
+                        "tiles -> own image -> every rank's image) + symmetric-memory barrier")
         else:
             par = f"pixel tiles x{world} (blocks of whole tile rows) + NCCL all_gather_into_tensor"
             step_txt = "sar_range_compress(all chirps) + sar_backproject(rank tile rows) + all_gather_into_tensor"
@@ -737,10 +770,11 @@ def main(argv=None):
                     help="N > 1: equal tile (row) counts per rank, no measured load balance")
     ap.add_argument("--all-legs", action="store_true",
                     help="N = 1 check run: a one-rank process group, both gather legs timed and checked")
-    ap.add_argument("--gather", default="auto", choices=["auto", "fused", "multicast", "nccl"],
+    ap.add_argument("--gather", default="auto", choices=["auto", "fused", "publish", "multicast", "nccl"],
                     help="N > 1, image configs: besides the NCCL all_gather leg (always timed), time the gather "
                          "fused into the BP epilogue (auto/fused: P2P stores, multicast: multimem.st to the "
-                         "NVSwitch multicast address; symmetric memory); nccl: the NCCL leg only.  C5: the "
+                         "NVSwitch multicast address; symmetric memory) and the publish leg (auto/publish: BP into "
+                         "the own image, then one copy of the tiles to the peers); nccl: the NCCL leg only.  C5: the "
                          "chirp-shard reduction is an NCCL reduce unless fused/multicast (P2P red.add)")
     args = ap.parse_args(argv)
     _claim_stdout()
@@ -772,7 +806,7 @@ def self_launch(args, argv):
     except Exception:
         ngpu = 0
     if ngpu < args.gpus:
-        legs = {"fused": None, "nccl": None}
+        legs = {"fused": None, "publish": None, "nccl": None}
         emit({"metric": METRIC if args.config not in ("C5", "C5i") else STREAM_METRIC, "value": None,
               "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
               "unavailable": f"--gpus {args.gpus}: {ngpu} GPU(s) visible",

@@ -212,6 +212,14 @@ sar_status_t sar_backproject(sar_plan_t plan, const sar_complex64_t* profiles,
  *   images  host array of n_images device pointers (may be peer or multicast addresses) */
 #define SAR_SCATTER_MULTICAST 1
 #define SAR_SCATTER_ADD 2
+/* sar_backproject_scatter_tiles only: compute first, then publish.  images[0] is the caller's OWN
+ * full image: the tiles are back-projected into it exactly as by sar_backproject_tiles (plain
+ * kernels, chirp chunks summed by the split-sum kernel), then one copy kernel stores the finished
+ * tiles at their absolute positions of images[1..n_images) (P2P stores over NVLink).  The copy
+ * does not overlap the compute but costs about one pass over the rank's pixels per peer, while
+ * the fused epilogue's split publish measured 4.5-6 % more BP time per rank (round 2).  Not with
+ * SAR_SCATTER_ADD or SAR_SCATTER_MULTICAST. */
+#define SAR_SCATTER_PUBLISH 4
 sar_status_t sar_backproject_scatter(sar_plan_t plan, const sar_complex64_t* profiles,
                                      const double* tx_pos, const double* rx_pos,
                                      const float* doppler_bins, int32_t chirp0, int32_t nchirp,

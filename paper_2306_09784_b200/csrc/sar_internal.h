@@ -116,6 +116,14 @@ struct SplitSumArgs {
   int planes, tile0, ntile, tiles_x, tile_y, row0, nrow, nx;
 };
 cudaError_t launch_split_sum(const SplitSumArgs& a, cudaStream_t s);
+// Publish (SAR_SCATTER_PUBLISH): copy the pixels of the absolute tiles [tile0, tile0 + ntile) of the
+// full image src to the same positions of every full image dst[d], d < n_dst.
+struct PublishArgs {
+  const float2* src;
+  float2* dst[8];
+  int n_dst, tile0, ntile, tiles_x, tile_y, nx, ny;
+};
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
 // Polar -> Cartesian resampling arguments (resample_kernel.cu).
 struct ResampleArgs {

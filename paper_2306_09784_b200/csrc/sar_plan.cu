@@ -926,7 +926,34 @@ sar_status_t sar_backproject_scatter_tiles(sar_plan_t plan, const sar_complex64_
   if (tile0 < 0) return fail(SAR_ERR_INVALID_ARGUMENT, "tile0 must be >= 0");
   if (!images || n_images < 1 || n_images > 8)
     return fail(SAR_ERR_INVALID_ARGUMENT, "images must hold 1..8 device pointers");
-  if (flags & ~(SAR_SCATTER_MULTICAST | SAR_SCATTER_ADD)) return fail(SAR_ERR_INVALID_ARGUMENT, "unknown flags");
+  if (flags & ~(SAR_SCATTER_MULTICAST | SAR_SCATTER_ADD | SAR_SCATTER_PUBLISH))
+    return fail(SAR_ERR_INVALID_ARGUMENT, "unknown flags");
+  if (flags & SAR_SCATTER_PUBLISH) {
+    if (flags & (SAR_SCATTER_MULTICAST | SAR_SCATTER_ADD))
+      return fail(SAR_ERR_INVALID_ARGUMENT, "SAR_SCATTER_PUBLISH stores only, to P2P images");
+    for (int d = 0; d < n_images; ++d)
+      if (!images[d]) return fail(SAR_ERR_INVALID_ARGUMENT, "null image pointer");
+    // the tiles into the caller's own image, then one copy of them to every other image
+    sar_status_t st = backproject_impl(plan, profiles, tx_pos, rx_pos, doppler_bins, chirp0, nchirp, 0, 0, images[0],
+                                       0, nullptr, 0, 0, stream, tile0, ntile);
+    if (st != SAR_OK || ntile == 0 || n_images == 1) return st;
+    DeviceGuard guard(plan->device);
+    const sar_grid_t& g = plan->grid;
+    sar::PublishArgs pa;
+    pa.src = reinterpret_cast<const float2*>(images[0]);
+    for (int d = 0; d < 8; ++d) pa.dst[d] = d + 1 < n_images ? reinterpret_cast<float2*>(images[d + 1]) : nullptr;
+    pa.n_dst = n_images - 1;
+    pa.tile0 = tile0;
+    pa.ntile = ntile;
+    pa.tiles_x = (g.nx + plan->info.tile_x - 1) / plan->info.tile_x;
+    pa.tile_y = plan->info.tile_y;
+    pa.nx = g.nx;
+    pa.ny = g.ny;
+    cudaError_t e = sar::launch_publish(pa, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "publish launch");
+    plan->launches.fetch_add(1);
+    return SAR_OK;
+  }
   const int multicast = (flags & SAR_SCATTER_MULTICAST) ? 1 : 0, add = (flags & SAR_SCATTER_ADD) ? 1 : 0;
   if (multicast && n_images != 1)
     return fail(SAR_ERR_INVALID_ARGUMENT, "a multicast store takes exactly one (multicast) address");

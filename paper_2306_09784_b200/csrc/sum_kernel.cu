@@ -60,7 +60,29 @@ __global__ void __launch_bounds__(256) split_sum_kernel(const SplitSumArgs a) {
   }
 }
 
+// One CTA per tile, one warp per 32-pixel tile row: every finished pixel is read once from the
+// local image and stored to each peer image (coalesced 256-B rows, P2P over NVLink).
+__global__ void __launch_bounds__(256) publish_kernel(const PublishArgs a) {
+  const int tile = a.tile0 + blockIdx.x;
+  const int i0 = (tile % a.tiles_x) * kTileX, J0 = (tile / a.tiles_x) * a.tile_y;
+  const int x = i0 + (threadIdx.x & 31);
+  if (x >= a.nx) return;
+  for (int yl = threadIdx.x >> 5; yl < a.tile_y; yl += blockDim.x >> 5) {
+    const int y = J0 + yl;
+    if (y >= a.ny) break;
+    const size_t o = (size_t)y * a.nx + x;
+    const float2 v = __ldcs(a.src + o);
+    for (int d = 0; d < a.n_dst; ++d) a.dst[d][o] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {
+  if (a.ntile <= 0 || a.n_dst <= 0) return cudaSuccess;
+  publish_kernel<<<(unsigned)a.ntile, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_split_sum(const SplitSumArgs& a, cudaStream_t s) {
   if (a.ntile <= 0) return cudaSuccess;

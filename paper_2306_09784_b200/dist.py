@@ -146,5 +146,11 @@ class FusedRowGather:
     def root_ptrs(self, root: int = 0):
         return [int(self.hdl.buffer_ptrs[root])]
 
+    def publish_ptrs(self, rank: int):
+        """The P2P buffers with the calling rank's own first (``SAR_SCATTER_PUBLISH``: compute into
+        the own image, then copy the finished tiles to the peers)."""
+        ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+        return [ptrs[rank]] + ptrs[:rank] + ptrs[rank + 1:]
+
     def barrier(self, channel: int = 0):
         self.hdl.barrier(channel=channel)

@@ -192,6 +192,7 @@ def sar_backproject(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row
 
 SAR_SCATTER_MULTICAST = 1
 SAR_SCATTER_ADD = 2
+SAR_SCATTER_PUBLISH = 4   # sar_backproject_scatter_tiles: compute into images[0], then copy to the others
 
 
 def sar_backproject_scatter(plan, prof_ptr, tx_ptr, rx_ptr, dop_ptr, chirp0, nchirp, row0, nrow, image_ptrs,
@@ -460,8 +461,10 @@ class Plan:
         return out
 
     def backproject_scatter_tiles(self, profiles, tx, image_ptrs, tile0, ntile, rx=None, doppler=None, chirp0=0,
-                                  nchirp=None, multicast=False, add=False, stream=None):
-        """``backproject_scatter`` over the absolute tiles [tile0, tile0+ntile)."""
+                                  nchirp=None, multicast=False, add=False, publish=False, stream=None):
+        """``backproject_scatter`` over the absolute tiles [tile0, tile0+ntile); ``publish``:
+        compute into image_ptrs[0] (the caller's own image), then copy the tiles to the others
+        (SAR_SCATTER_PUBLISH)."""
         import torch
 
         g = self.grid
@@ -473,7 +476,8 @@ class Plan:
                                       _dptr(rx, torch.float64, (self.n_chirps, self.n_rx, 3), "rx"),
                                       _dptr(doppler, torch.float32, (g.ny, g.nx), "doppler"),
                                       chirp0, nchirp, tile0, ntile, [int(p) for p in image_ptrs],
-                                      (SAR_SCATTER_MULTICAST if multicast else 0) | (SAR_SCATTER_ADD if add else 0),
+                                      (SAR_SCATTER_MULTICAST if multicast else 0) | (SAR_SCATTER_ADD if add else 0)
+                                      | (SAR_SCATTER_PUBLISH if publish else 0),
                                       _stream_handle(stream))
 
     def form_image(self, raw_h, tx_h, rx_h=None, wsar_h=None, doppler_h=None, row0=0, nrow=None, out_h=None,

@@ -73,15 +73,19 @@ def test_gather_summary_picks_the_fastest_verified_leg():
     assert g["headline"] == "nccl"
     g = bench.gather_summary(2, {"fused": None, "nccl": legs["nccl"]}, {"nccl": {"ok": False}})
     assert g["headline"] is None and g["fused_ms"] is None
+    legs["publish"] = {"ms": 7.5, "bp_ms": [7.4, 7.3], "collective_ms": [0.1, 0.1]}
+    g = bench.gather_summary(2, legs, {"fused": {"ok": True}, "publish": {"ok": True}, "nccl": {"ok": True}})
+    assert g["headline"] == "publish" and g["publish_ms"] == 7.5
 
 
 @pytest.mark.gpu
 def test_both_gather_legs_on_one_rank():
     """--all-legs: the N > 1 code path on a one-rank group (symmetric-memory fused scatter of the
-    rank's tile block, NCCL all-gather of its tile rows), both legs timed and checked against the
-    1-GPU image; exactly one JSON line on stdout."""
+    rank's tile block, the publish leg, NCCL all-gather of its tile rows), every leg timed and checked
+    against the 1-GPU image; exactly one JSON line on stdout."""
     d = _run(["--config", "C0", "--all-legs", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"], 900)
     g = d["gather"]
-    assert g["world"] == 1 and g["headline"] in ("fused", "nccl")
-    assert g["fused_check"]["ok"] and g["nccl_check"]["ok"]
+    assert g["world"] == 1 and g["headline"] in ("fused", "publish", "nccl")
+    assert g["fused_check"]["ok"] and g["nccl_check"]["ok"] and g["publish_check"]["ok"]
+    assert g["publish_ms"] > 0
     assert g["fused_ms"] > 0 and g["nccl_ms"] > 0 and len(g["fused_bp_ms_per_rank"]) == 1

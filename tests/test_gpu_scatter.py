@@ -163,3 +163,39 @@ def test_tile_scatter_equals_tile_backproject(cuda_lib):
     for im in imgs:
         assert torch.equal(im, ref)
     plan.close()
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_publish_scatter_equals_tile_backproject(cuda_lib, big):
+    """SAR_SCATTER_PUBLISH: the tiles are computed into images[0] like sar_backproject_tiles (bit for
+    bit), then copied to images[1..]; other pixels untouched.  ``big``: a C3 tile block whose launch
+    splits its chirps (chunk planes + split sum before the copy), ragged last tile row included."""
+    import torch
+
+    from paper_2306_09784_b200 import sar
+
+    if big:
+        scn = sarsim.make_config("C3")
+        raw = sarsim.simulate_raw(scn, device="cuda:0")
+        lo, hi = scn.antenna_box(1e-3)
+        plan = sar.Plan(scn.radar, scn.grid, scn.n_chirps, scn.n_rx, (lo, hi))
+        tx = torch.as_tensor(scn.tx, device="cuda:0")
+        prof = plan.range_compress(raw)
+        tiles_x, tiles_y = plan.tiles
+        t0, nt = tiles_x * tiles_y - 1111, 1111   # the last 1111 tiles: ragged last row and column
+    else:
+        scn, plan, tx, prof = _setup(cuda_lib)
+        t0, nt = 2, 3
+    g = scn.grid
+    sentinel = complex(7.0, -7.0)
+    ref = torch.full((g.ny, g.nx), sentinel, dtype=torch.complex64, device="cuda:0")
+    plan.backproject_tiles(prof, tx, t0, nt, out=ref)
+    imgs = [torch.full((g.ny, g.nx), sentinel, dtype=torch.complex64, device="cuda:0") for _ in range(3)]
+    plan.backproject_scatter_tiles(prof, tx, [im.data_ptr() for im in imgs], t0, nt, publish=True)
+    torch.cuda.synchronize()
+    assert int((ref != sentinel).sum()) > 0
+    for im in imgs:
+        assert torch.equal(im, ref)
+    with pytest.raises(sar.SarError):
+        plan.backproject_scatter_tiles(prof, tx, [imgs[0].data_ptr()], t0, nt, publish=True, add=True)
+    plan.close()

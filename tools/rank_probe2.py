@@ -48,20 +48,27 @@ for world in worlds:
     ideal = t1 / world
     # bench.py's measured load balance: equal blocks, then two re-cuts on the measured block times
     tb = [tile_partition(tiles_x * tiles_y, world, r) for r in range(world)]
+    pb = list(tb)
     rb = [row_partition(tiles_y, world, r) for r in range(world)]
     ty = plan.info.tile_y
     for it in range(3):
         fused = [timed(lambda: plan.backproject_scatter_tiles(prof, tx, ptrs, t0, nt, rx)) for t0, nt in tb]
+        pub = [timed(lambda: plan.backproject_scatter_tiles(prof, tx, ptrs, t0, nt, rx, publish=True)) for t0, nt in pb]
+        if os.environ.get("PROBE_PLAIN_TILES"):   # the same tile blocks through the plain family
+            plain = [timed(lambda: plan.backproject_tiles(prof, tx, t0, nt, rx, out=imgs[0])) for t0, nt in tb]
+            print(f"N={world} it{it}: plain tile blocks per rank {['%.3f' % t for t in plain]} max {max(plain):.3f} "
+                  f"({max(plain) / ideal:.3f} x ideal)")
         rows = []
         for a, n in rb:
             row0, nrow = min(g.ny, a * ty), min(g.ny, (a + n) * ty) - min(g.ny, a * ty)
             out = torch.empty((max(nrow, 1), g.nx), dtype=torch.complex64, device=dev)
             rows.append(timed(lambda: plan.backproject(prof, tx, rx, row0=row0, nrow=nrow, out=out[:nrow])))
         label = "equal blocks" if it == 0 else f"rebalanced x{it}"
-        for name, ts in (("fused (tile blocks)", fused), ("NCCL leg (tile rows)", rows)):
+        for name, ts in (("fused (tile blocks)", fused), ("publish (tile blocks)", pub), ("NCCL leg (tile rows)", rows)):
             print(f"N={world} {label}: {name} per rank {['%.3f' % t for t in ts]} max {max(ts):.3f} "
                   f"({max(ts) / ideal:.3f} x ideal, spread {(max(ts) - min(ts)) / max(ts):.1%})")
         tb = [rebalance(tb, fused, world, r) for r in range(world)]
+        pb = [rebalance(pb, pub, world, r) for r in range(world)]
         rb = [rebalance(rb, rows, world, r) for r in range(world)]
     del imgs
 plan.close()
