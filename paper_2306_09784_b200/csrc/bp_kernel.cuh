@@ -176,6 +176,10 @@ constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
 // blocks N = 2: 28.44 ms unsplit (7.5 waves) -> 27.80 split; N = 8: 7.13 (32 waves) -> 7.09; C3 e2e
 // (host image) 56.62 -> 55.86 ms
 constexpr long kScatterWaves = 16;
+#ifndef SAR_BP_L2_WINDOW_MB
+#define SAR_BP_L2_WINDOW_MB 40   // pair-row bytes of one chirp chunk at most (126 MB L2 on two dies)
+#endif
+constexpr long kL2WindowMB = SAR_BP_L2_WINDOW_MB;
 constexpr long kScatterUnsplit = 1L << 40;   // (a depth at which a scatter would run unsplit: none)
 inline long env_long(const char* name, long dflt) {
   const char* e = getenv(name);
@@ -1325,6 +1329,14 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   while (ntiles * k < waves * slots && (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems &&
          a.nchirp / (2 * k) >= a.CB)
     k *= 2;
+  // ... and enough chunks that one chunk's pair rows (the rows the resident CTAs stream at a time,
+  // chunk-major order) stay well inside L2: C4's 750-row rank block at 3 CTAs per SM took k = 4
+  // (92 MB per chunk) and read 5.7 GB from DRAM per launch instead of the rows' ~0.4 GB
+  static const long l2_window = env_long("SAR_BP_L2_WINDOW_MB", kL2WindowMB) << 20;
+  if (a.pairs && !(a.n_peer > 0 && a.accumulate))
+    while ((long)((a.nchirp + k - 1) / k) * a.n_rx * a.pair_stride * 16L > l2_window &&
+           (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems && a.nchirp / (2 * k) >= a.CB)
+      k *= 2;
   if (a.n_peer > 0 && ntiles >= scatter_unsplit * slots) k = 1;
   // reductions into peers (chirp shards) run unsplit
   if (a.n_peer > 0 && a.accumulate) k = 1;
