@@ -1332,8 +1332,11 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
   // ... and enough chunks that one chunk's pair rows (the rows the resident CTAs stream at a time,
   // chunk-major order) stay well inside L2: C4's 750-row rank block at 3 CTAs per SM took k = 4
   // (92 MB per chunk) and read 5.7 GB from DRAM per launch instead of the rows' ~0.4 GB
+  // (plain launches only: a scatter -- the fused gather, sar_form_image's host-image stores -- keeps
+  //  its unsplit epilogue stores where the waves allow; forcing C3's host-image launch to 8 chunks
+  //  cost 1.3 ms end to end)
   static const long l2_window = env_long("SAR_BP_L2_WINDOW_MB", kL2WindowMB) << 20;
-  if (a.pairs && !(a.n_peer > 0 && a.accumulate))
+  if (a.pairs && a.n_peer == 0)
     while ((long)((a.nchirp + k - 1) / k) * a.n_rx * a.pair_stride * 16L > l2_window &&
            (long)a.nchirp * a.n_rx / (2 * k) >= kMinSplitItems && a.nchirp / (2 * k) >= a.CB)
       k *= 2;
