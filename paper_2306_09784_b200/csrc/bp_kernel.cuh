@@ -177,7 +177,7 @@ constexpr long kSplitWaves = SAR_BP_SPLIT_WAVES;
 // (host image) 56.62 -> 55.86 ms
 constexpr long kScatterWaves = 16;
 #ifndef SAR_BP_L2_WINDOW_MB
-#define SAR_BP_L2_WINDOW_MB 40   // pair-row bytes of one chirp chunk at most (126 MB L2 on two dies)
+#define SAR_BP_L2_WINDOW_MB 64   // pair-row bytes of one chirp chunk at most (126 MB L2 on two dies)
 #endif
 constexpr long kL2WindowMB = SAR_BP_L2_WINDOW_MB;
 constexpr long kScatterUnsplit = 1L << 40;   // (a depth at which a scatter would run unsplit: none)
@@ -1330,8 +1330,10 @@ cudaError_t launch_one(const BpArgs& a, cudaStream_t s) {
          a.nchirp / (2 * k) >= a.CB)
     k *= 2;
   // ... and enough chunks that one chunk's pair rows (the rows the resident CTAs stream at a time,
-  // chunk-major order) stay well inside L2: C4's 750-row rank block at 3 CTAs per SM took k = 4
-  // (92 MB per chunk) and read 5.7 GB from DRAM per launch instead of the rows' ~0.4 GB
+  // chunk-major order) stay inside L2: C4's 750-row rank block at 3 CTAs per SM took k = 4 (92 MB
+  // per chunk) and read 5.7 GB from DRAM per launch instead of the rows' ~0.4 GB.  Window 40 / 64 MB
+  // (tools/gpu_r4s.sh): C3 50.00 / 49.89 ms with 0.76 / 0.49 GB of DRAM traffic (chunk planes), C4
+  // 868.5 / 870.4 ms, C4 rank block 111.9 / 112.9 ms
   // (plain launches only: a scatter -- the fused gather, sar_form_image's host-image stores -- keeps
   //  its unsplit epilogue stores where the waves allow; forcing C3's host-image launch to 8 chunks
   //  cost 1.3 ms end to end)
