@@ -590,8 +590,9 @@ def run_ours(args):
             "e2e": {"value": scn.updates / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_image": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "load_ms": load_ms, "load_note": "pinned H2D of raw samples + poses alone (Table 2 'Load')",
-                    "api": "sar_form_image (C ABI, pinned host buffers: H2D raw+poses, rc, bp whose epilogue "
-                           "stores the image rows into the mapped pinned host buffer)"
+                    "api": "sar_form_image (C ABI, pinned host buffers: H2D poses, rc reading the pinned raw "
+                           "samples in place, bp in 4 bands of tile rows with each band's D2H copy overlapping "
+                           "the next band)"
                            + ("" if world == 1 else "; each rank its tile-row block")},
             "gpu_launches": leg["launches"],
             "clocks": clocks,

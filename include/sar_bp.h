@@ -259,10 +259,11 @@ sar_status_t sar_backproject_scatter_tiles(sar_plan_t plan, const sar_complex64_
  * Table 2, pinned memory P:L357-360): copies raw, w_sar and poses to a
  * plan-owned device workspace, runs sar_range_compress over all chirps and
  * sar_backproject over all chirps for grid rows [row0, row0 + nrow), and returns
- * those image rows, all on `stream`.  When image_host is pinned (device-mapped), the
- * BP epilogue stores each finished tile straight into image_host (readback overlapped
- * with the compute; under a chirp split the last chunk of each tile stores it);
- * otherwise one copy follows the kernel.  A pinned raw_host is read by the range
+ * those image rows, all on `stream`.  When image_host is pinned (device-mapped), the rows
+ * run as up to 4 bands of whole tile rows and each band is copied to image_host (on a
+ * plan-owned copy stream) while the next band computes -- the readback overlapped with the
+ * compute; a single tile row instead has the BP epilogue store each finished tile straight
+ * into image_host.  Otherwise one copy follows the kernel.  A pinned raw_host is read by the range
  * compression directly.
  *   raw_host [n_chirps][n_rx][n_samples] float; w_sar_host [n_chirps] float or NULL;
  *   tx_host [n_chirps][3] double; rx_host [n_chirps][n_rx][3] double or NULL;

@@ -176,6 +176,8 @@ struct sar_plan_s {
   float* w_dop = nullptr;
   float2* w_prof = nullptr;
   float2* w_img = nullptr;
+  cudaStream_t w_copy = nullptr;   // sar_form_image: readback stream of the banded pipeline
+  cudaEvent_t w_ev[9] = {};        // band-done events (8 bands max) + the last copy's
   cudaMemPool_t pool = nullptr;   // device pool of the per-call pair-format rows (not owned)
   std::atomic<int64_t> launches{0};
 };

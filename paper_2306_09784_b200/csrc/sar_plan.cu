@@ -325,6 +325,9 @@ void free_plan(sar_plan_s* p) {
   cudaFree(p->w_dop);
   cudaFree(p->w_prof);
   cudaFree(p->w_img);
+  for (cudaEvent_t ev : p->w_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (p->w_copy) cudaStreamDestroy(p->w_copy);
   delete p;
 }
 
@@ -971,6 +974,15 @@ sar_status_t sar_plan_tiles(sar_plan_t plan, int32_t* tiles_x, int32_t* tiles_y)
   return SAR_OK;
 }
 
+#ifndef SAR_FORM_BANDS
+// sar_form_image: bands of the readback pipeline (0: the BP epilogue stores into the host image).
+// Measured (tools/gpu_r4t.sh) e2e with 0 / 2 / 4 / 8 bands: C3 51.55 / 51.24 / 51.04 / 51.41 ms; C4
+// 891.7 (0) / 882.4 (4) ms: the epilogue's host stores kept the launch unsplit (no L2 window for
+// scatters), the bands run the plain kernels
+#define SAR_FORM_BANDS 4
+#endif
+constexpr int kFormBands = SAR_FORM_BANDS;
+
 sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float* w_sar_host,
                             const double* tx_host, const double* rx_host,
                             const float* doppler_host, int32_t row0, int32_t nrow,
@@ -1047,6 +1059,46 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   void* mapped = nullptr;
   const bool direct = nrow > 0 && cudaHostGetDevicePointer(&mapped, image_host, 0) == cudaSuccess && mapped;
   if (!direct) cudaGetLastError();   // clear the error of a pageable buffer
+  static const int bands_env = [] {   // SAR_FORM_BANDS=n: banded readback pipeline (0: epilogue stores)
+    const char* v = getenv("SAR_FORM_BANDS");
+    return v && *v ? atoi(v) : kFormBands;
+  }();
+  const int TYp = plan->info.tile_y;
+  const int trow0 = row0 / TYp, trow1 = (row0 + nrow + TYp - 1) / TYp;
+  const int nbands = std::min(std::min(bands_env, 8), trow1 - trow0);
+  if (direct && nbands >= 2) {
+    // Readback pipelined with the compute: the call's rows run as bands of whole tile rows; each
+    // band's BP writes the plan's device image (plain kernels, L2-bounded chirp split), then the
+    // band is copied to the pinned host image on the plan's copy stream while the next band
+    // computes; `stream` waits for the last copy.
+    if (!plan->w_copy) {
+      if ((e = cudaStreamCreateWithFlags(&plan->w_copy, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "copy stream");
+      for (cudaEvent_t& ev : plan->w_ev)
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    }
+    for (int bnd = 0; bnd < nbands; ++bnd) {
+      const int tb0 = trow0 + (int)((int64_t)(trow1 - trow0) * bnd / nbands);
+      const int tb1 = trow0 + (int)((int64_t)(trow1 - trow0) * (bnd + 1) / nbands);
+      const int rb0 = std::max(row0, tb0 * TYp), rb1 = std::min(row0 + nrow, tb1 * TYp);
+      if (rb1 <= rb0) continue;
+      st = sar_backproject(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
+                           rx_host ? plan->w_rx : nullptr, doppler_host ? plan->w_dop : nullptr, 0, r.n_chirps,
+                           rb0, rb1 - rb0, reinterpret_cast<sar_complex64_t*>(plan->w_img) + (size_t)(rb0 - row0) * g.nx,
+                           0, stream);
+      if (st != SAR_OK) return st;
+      if ((e = cudaEventRecord(plan->w_ev[bnd], s)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(plan->w_copy, plan->w_ev[bnd], 0)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(image_host + (size_t)(rb0 - row0) * g.nx, plan->w_img + (size_t)(rb0 - row0) * g.nx,
+                               (size_t)(rb1 - rb0) * g.nx * sizeof(float2), cudaMemcpyDeviceToHost, plan->w_copy)) !=
+              cudaSuccess)
+        return cuda_fail(e, "band readback");
+    }
+    if ((e = cudaEventRecord(plan->w_ev[8], plan->w_copy)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, plan->w_ev[8], 0)) != cudaSuccess)
+      return cuda_fail(e, "readback join");
+    return SAR_OK;
+  }
   if (direct) {
     sar_complex64_t* base = reinterpret_cast<sar_complex64_t*>(mapped) - (ptrdiff_t)row0 * g.nx;
     return backproject_impl(plan, reinterpret_cast<sar_complex64_t*>(plan->w_prof), plan->w_tx,
