@@ -1065,7 +1065,13 @@ sar_status_t sar_form_image(sar_plan_t plan, const float* raw_host, const float*
   }();
   const int TYp = plan->info.tile_y;
   const int trow0 = row0 / TYp, trow1 = (row0 + nrow + TYp - 1) / TYp;
-  const int nbands = std::min(std::min(bands_env, 8), trow1 - trow0);
+  // bands only where each still fills the GPU twice over (~3 resident CTAs per SM): small grids
+  // lose more to per-band tails than the overlap saves (C0 / C6, 1444 tiles: e2e +1.4 % / +5 %)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+  const int64_t call_tiles = (int64_t)(trow1 - trow0) * ((g.nx + plan->info.tile_x - 1) / plan->info.tile_x);
+  const int nbands = (int)std::min<int64_t>(std::min(std::min(bands_env, 8), trow1 - trow0),
+                                            call_tiles / (2 * 3 * (int64_t)sms));
   if (direct && nbands >= 2) {
     // Readback pipelined with the compute: the call's rows run as bands of whole tile rows; each
     // band's BP writes the plan's device image (plain kernels, L2-bounded chirp split), then the
